@@ -1,0 +1,449 @@
+// Pointwise spectral operators on cuFFT half spectra (proj/src/spectral.cpp).
+//
+// One fused pass per operator over all components of the half spectrum
+// n1 x n2 x (n3/2+1): the symbol, the 1/N inverse normalisation
+// (fft.cpp:56-64) and any cross-component coupling (Leray) are applied in a
+// single read+write of the spectrum. Forward R2C / inverse C2R are batched
+// over the 3 components (one plan each, shared work area) and timed as
+// "fft" (counters.hpp:69-78).
+//
+// Spectral element addressing is written against a slab descriptor
+// (k1 all, k2 in [k2off, k2off + n2l), k3 half) so the same symbol kernels
+// run on the x2-slab layout of the distributed transform (dist.cu).
+#include <cmath>
+
+#include "common.cuh"
+
+namespace vb {
+
+struct SpecDesc {
+  int n1, n2, n3, h;  // h = n3/2 + 1
+  int n2l, k2off;     // local k2 range
+  size_t nc;          // local complex elements per component
+};
+
+__device__ __forceinline__ void spec_index(const SpecDesc& d, size_t e, int& k1, int& k2, int& k3) {
+  k3 = int(e % size_t(d.h));
+  const size_t r = e / size_t(d.h);
+  k2 = int(r % size_t(d.n2l)) + d.k2off;
+  k1 = int(r / size_t(d.n2l));
+}
+
+__device__ __forceinline__ float sfreq(int k, int n) { return float(k <= n / 2 ? k : k - n); }
+
+namespace {
+
+constexpr unsigned kT = 256;
+
+// F *= scale * sym(k), sym = beta |k|^2 (zero mode: unit or 0) [regop] or
+// 1 / (beta |k|^2) (zero mode 1/beta) [inv_regop] (spectral.cpp:48-93).
+__global__ void k_symbol(SpecDesc d, int ncomp, float2* __restrict__ F, float beta, int inverse,
+                         int unit_zero, float scale) {
+  const size_t total = d.nc * size_t(ncomp);
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    int k1, k2, k3;
+    spec_index(d, e % d.nc, k1, k2, k3);
+    const float f1 = sfreq(k1, d.n1), f2 = sfreq(k2, d.n2), f3 = float(k3);
+    float sym = f1 * f1 + f2 * f2 + f3 * f3;
+    float m;
+    if (inverse) {
+      if (sym == 0.0f) sym = 1.0f;
+      m = scale / (beta * sym);
+    } else {
+      if (sym == 0.0f) sym = unit_zero ? 1.0f : 0.0f;
+      m = scale * (beta * sym);
+    }
+    float2 v = F[e];
+    v.x *= m;
+    v.y *= m;
+    F[e] = v;
+  }
+}
+
+// Leray: F_c -= f_c (f . F)/|k|^2, zero mode untouched (spectral.cpp:120-147).
+__global__ void k_leray(SpecDesc d, float2* __restrict__ F, float scale) {
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < d.nc; e += stride) {
+    int k1, k2, k3;
+    spec_index(d, e, k1, k2, k3);
+    const float f1 = sfreq(k1, d.n1), f2 = sfreq(k2, d.n2), f3 = float(k3);
+    const float ksq = f1 * f1 + f2 * f2 + f3 * f3;
+    float2 a = F[e], b = F[d.nc + e], c = F[2 * d.nc + e];
+    if (ksq != 0.0f) {
+      const float kvx = (f1 * a.x + f2 * b.x + f3 * c.x) / ksq;
+      const float kvy = (f1 * a.y + f2 * b.y + f3 * c.y) / ksq;
+      a.x -= f1 * kvx; a.y -= f1 * kvy;
+      b.x -= f2 * kvx; b.y -= f2 * kvy;
+      c.x -= f3 * kvx; c.y -= f3 * kvy;
+    }
+    a.x *= scale; a.y *= scale; b.x *= scale; b.y *= scale; c.x *= scale; c.y *= scale;
+    F[e] = a;
+    F[d.nc + e] = b;
+    F[2 * d.nc + e] = c;
+  }
+}
+
+// Per-(component, k2-row) fp64 partial of sum w3 |k|^2 |F|^2 over k3, k1
+// (spectral.cpp:95-118: k2-major fold).
+__global__ void k_seminorm_rows(SpecDesc d, const float2* __restrict__ F, double* __restrict__ rows) {
+  const int c = blockIdx.y;
+  const int k2l = blockIdx.x;
+  const int k2 = k2l + d.k2off;
+  const float f2 = sfreq(k2, d.n2);
+  const float2* Fc = F + size_t(c) * d.nc;
+  double acc = 0.0;
+  const int cnt = d.n1 * d.h;
+  for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+    const int k1 = t / d.h, k3 = t % d.h;
+    const float f1 = sfreq(k1, d.n1);
+    const double w3 = (k3 == 0 || 2 * k3 == d.n3) ? 1.0 : 2.0;
+    const double sym = double(f1) * f1 + double(f2) * f2 + double(k3) * k3;
+    const float2 v = Fc[(size_t(k1) * d.n2l + k2l) * d.h + k3];
+    acc += w3 * sym * (double(v.x) * v.x + double(v.y) * v.y);
+  }
+  __shared__ double sh[kT];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (unsigned s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) rows[size_t(c) * d.n2l + k2l] = sh[0];
+}
+
+// Full-space lookup of a half spectrum (fft.hpp:35-43).
+__device__ __forceinline__ float2 full_at(const float2* F, int n1, int n2, int n3, int k1, int k2,
+                                          int k3) {
+  const int h = n3 / 2 + 1;
+  if (k3 <= n3 / 2) return F[(size_t(k1) * n2 + k2) * h + k3];
+  const int m1 = (n1 - k1) % n1, m2 = (n2 - k2) % n2, m3 = n3 - k3;
+  float2 v = F[(size_t(m1) * n2 + m2) * h + m3];
+  v.y = -v.y;
+  return v;
+}
+
+__device__ __forceinline__ int pmod(int a, int n) {
+  a %= n;
+  return a < 0 ? a + n : a;
+}
+
+// Coarse half spectrum from the fine one: partner sums on the coarse
+// Nyquist lines, times scale (spectral.cpp:149-174).
+__global__ void k_restrict(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3, int ncomp,
+                           const float2* __restrict__ Ff, float2* __restrict__ Fc, float scale) {
+  const int hc = nc3 / 2 + 1, hf = nf3 / 2 + 1;
+  const size_t ncc = size_t(nc1) * nc2 * hc, ncf = size_t(nf1) * nf2 * hf;
+  const size_t total = ncc * size_t(ncomp);
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int c = int(e / ncc);
+    const size_t r = e % ncc;
+    const int k3 = int(r % hc), k2 = int((r / hc) % nc2), k1 = int(r / (size_t(hc) * nc2));
+    const int nu1 = k1 <= nc1 / 2 ? k1 : k1 - nc1;
+    const int nu2 = k2 <= nc2 / 2 ? k2 : k2 - nc2;
+    const int nu3 = k3;
+    int p1[2] = {nu1, 0}, p2[2] = {nu2, 0}, p3[2] = {nu3, 0};
+    int c1 = 1, c2 = 1, c3 = 1;
+    if (abs(nu1) == nc1 / 2) { p1[0] = nc1 / 2; p1[1] = -nc1 / 2; c1 = 2; }
+    if (abs(nu2) == nc2 / 2) { p2[0] = nc2 / 2; p2[1] = -nc2 / 2; c2 = 2; }
+    if (abs(nu3) == nc3 / 2) { p3[0] = nc3 / 2; p3[1] = -nc3 / 2; c3 = 2; }
+    const float2* F = Ff + size_t(c) * ncf;
+    float ax = 0.f, ay = 0.f;
+    for (int a = 0; a < c1; ++a)
+      for (int b = 0; b < c2; ++b)
+        for (int q = 0; q < c3; ++q) {
+          const float2 v = full_at(F, nf1, nf2, nf3, pmod(p1[a], nf1), pmod(p2[b], nf2),
+                                   pmod(p3[q], nf3));
+          ax += v.x;
+          ay += v.y;
+        }
+    Fc[e] = make_float2(ax * scale, ay * scale);
+  }
+}
+
+// Fine half spectrum from the coarse one: coarse modes split evenly over
+// their fine partners, zero outside the band (spectral.cpp:176-203).
+__global__ void k_prolong(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3, int ncomp,
+                          const float2* __restrict__ Fc, float2* __restrict__ Ff, float scale) {
+  const int hc = nc3 / 2 + 1, hf = nf3 / 2 + 1;
+  const size_t ncc = size_t(nc1) * nc2 * hc, ncf = size_t(nf1) * nf2 * hf;
+  const size_t total = ncf * size_t(ncomp);
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int c = int(e / ncf);
+    const size_t r = e % ncf;
+    const int f3 = int(r % hf), f2 = int((r / hf) % nf2), f1 = int(r / (size_t(hf) * nf2));
+    const int nu1 = f1 <= nf1 / 2 ? f1 : f1 - nf1;
+    const int nu2 = f2 <= nf2 / 2 ? f2 : f2 - nf2;
+    float2 out = make_float2(0.f, 0.f);
+    if (abs(nu1) <= nc1 / 2 && abs(nu2) <= nc2 / 2 && f3 <= nc3 / 2) {
+      const int cnt = (abs(nu1) == nc1 / 2 ? 2 : 1) * (abs(nu2) == nc2 / 2 ? 2 : 1) *
+                      (f3 == nc3 / 2 ? 2 : 1);
+      const float2 v = Fc[size_t(c) * ncc + (size_t(pmod(nu1, nc1)) * nc2 + pmod(nu2, nc2)) * hc + f3];
+      const float m = scale / float(cnt);
+      out = make_float2(v.x * m, v.y * m);
+    }
+    Ff[e] = out;
+  }
+}
+
+// High pass with the alias-pair remainder on the coarse Nyquist lines
+// (spectral.cpp:205-240); out of place (reads the original spectrum).
+__global__ void k_high_pass(int n1, int n2, int n3, int ncomp, const float2* __restrict__ Fin,
+                            float2* __restrict__ Fout, float scale) {
+  const int h = n3 / 2 + 1;
+  const size_t nc = size_t(n1) * n2 * h;
+  const size_t total = nc * size_t(ncomp);
+  const int b1 = n1 / 4, b2 = n2 / 4, b3 = n3 / 4;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int c = int(e / nc);
+    const size_t r = e % nc;
+    const int k3 = int(r % h), k2 = int((r / h) % n2), k1 = int(r / (size_t(h) * n2));
+    const int nu1 = k1 <= n1 / 2 ? k1 : k1 - n1;
+    const int nu2 = k2 <= n2 / 2 ? k2 : k2 - n2;
+    const float2* F = Fin + size_t(c) * nc;
+    float2 v = F[r];
+    if (!(abs(nu1) > b1 || abs(nu2) > b2 || k3 > b3)) {
+      const bool y1 = abs(nu1) == b1, y2 = abs(nu2) == b2, y3 = k3 == b3;
+      if (!y1 && !y2 && !y3) {
+        v = make_float2(0.f, 0.f);
+      } else {
+        float ax = 0.f, ay = 0.f;
+        int cnt = 0;
+        for (int s1 = 0; s1 < (y1 ? 2 : 1); ++s1)
+          for (int s2 = 0; s2 < (y2 ? 2 : 1); ++s2)
+            for (int s3 = 0; s3 < (y3 ? 2 : 1); ++s3) {
+              const int m1 = y1 ? (s1 ? n1 - b1 : b1) : k1;
+              const int m2 = y2 ? (s2 ? n2 - b2 : b2) : k2;
+              const int m3 = y3 ? (s3 ? n3 - b3 : b3) : k3;
+              const float2 w = full_at(F, n1, n2, n3, m1, m2, m3);
+              ax += w.x;
+              ay += w.y;
+              ++cnt;
+            }
+        v.x -= ax / float(cnt);
+        v.y -= ay / float(cnt);
+      }
+    }
+    Fout[e] = make_float2(v.x * scale, v.y * scale);
+  }
+}
+
+// out_c += g_c (g . s) (precond.hpp:36-37)
+__global__ void k_h0_pointwise(size_t n, const float* __restrict__ s, const float* __restrict__ g,
+                               float* __restrict__ out) {
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += stride) {
+    const float g1 = g[p], g2 = g[n + p], g3 = g[2 * n + p];
+    const float dot = g1 * s[p] + g2 * s[n + p] + g3 * s[2 * n + p];
+    out[p] += dot * g1;
+    out[n + p] += dot * g2;
+    out[2 * n + p] += dot * g3;
+  }
+}
+
+}  // namespace
+
+// ---- transform plumbing (single rank: cuFFT 3-D; multi-rank: dist.cu) ----
+
+SpecDesc spec_desc(vreg_ctx ctx, const Slab& s) {
+  SpecDesc d;
+  d.n1 = s.n1;
+  d.n2 = s.n2;
+  d.n3 = s.n3;
+  d.h = s.n3 / 2 + 1;
+  d.n2l = s.n2 / ctx->nranks;
+  d.k2off = ctx->rank * d.n2l;
+  d.nc = size_t(s.n1) * d.n2l * d.h;
+  return d;
+}
+
+void dist_fft_forward(vreg_ctx ctx, const Slab& s, int ncomp, const float* f, float2* F);
+void dist_fft_inverse(vreg_ctx ctx, const Slab& s, int ncomp, float2* F, float* f);
+
+float2* spec_buffer(vreg_ctx ctx, const SpecDesc& d, int ncomp, const char* name) {
+  return static_cast<float2*>(workspace(ctx, name, d.nc * size_t(ncomp) * sizeof(float2)));
+}
+
+void fft_forward(vreg_ctx ctx, const Slab& s, int ncomp, const float* f, float2* F) {
+  Timed t(ctx, T_FFT);
+  if (ctx->nranks > 1) {
+    dist_fft_forward(ctx, s, ncomp, f, F);
+    return;
+  }
+  FftPlans& p = fft_plans(ctx, s.n1, s.n2, s.n3, ncomp);
+  VB_CUFFT(cufftExecR2C(p.r2c, const_cast<float*>(f), reinterpret_cast<cufftComplex*>(F)));
+}
+
+void fft_inverse(vreg_ctx ctx, const Slab& s, int ncomp, float2* F, float* f) {
+  Timed t(ctx, T_FFT);
+  if (ctx->nranks > 1) {
+    dist_fft_inverse(ctx, s, ncomp, F, f);
+    return;
+  }
+  FftPlans& p = fft_plans(ctx, s.n1, s.n2, s.n3, ncomp);
+  VB_CUFFT(cufftExecC2R(p.c2r, reinterpret_cast<cufftComplex*>(F), f));
+}
+
+void apply_symbol(vreg_ctx ctx, const SpecDesc& d, int ncomp, float2* F, double beta, bool inverse,
+                  bool unit_zero, double scale) {
+  k_symbol<<<blocks_for(d.nc * ncomp, kT), kT, 0, ctx->stream>>>(
+      d, ncomp, F, float(beta), inverse ? 1 : 0, unit_zero ? 1 : 0, float(scale));
+  count_launch(ctx);
+  check_launch();
+}
+
+// out3 = beta A v3 (or its inverse); used by the fused matvec too.
+void spectral_regop(vreg_ctx ctx, const Slab& s, const float* v3, double beta, bool unit_zero,
+                    bool inverse, float* out3) {
+  require(beta > 0.0, VREG_EPARAM, "regularization beta must be > 0");
+  const SpecDesc d = spec_desc(ctx, s);
+  float2* F = spec_buffer(ctx, d, 3, "spec3");
+  fft_forward(ctx, s, 3, v3, F);
+  apply_symbol(ctx, d, 3, F, beta, inverse, unit_zero, 1.0 / double(s.global()));
+  fft_inverse(ctx, s, 3, F, out3);
+}
+
+void h0_pointwise(vreg_ctx ctx, const Slab& s, const float* s3, const float* g3, float* out3) {
+  k_h0_pointwise<<<blocks_for(s.local(), kT), kT, 0, ctx->stream>>>(s.local(), s3, g3, out3);
+  count_launch(ctx);
+  check_launch();
+}
+
+}  // namespace vb
+
+using namespace vb;
+
+extern "C" {
+
+int vreg_regop(vreg_ctx ctx, const vreg_grid* g, const float* v3, double beta, int unit_zero,
+               float* out3) {
+  return guard([&] { spectral_regop(ctx, slab_of(ctx, g), v3, beta, unit_zero != 0, false, out3); });
+}
+
+int vreg_inv_regop(vreg_ctx ctx, const vreg_grid* g, const float* v3, double beta, float* out3) {
+  return guard([&] { spectral_regop(ctx, slab_of(ctx, g), v3, beta, true, true, out3); });
+}
+
+int vreg_seminorm(vreg_ctx ctx, const vreg_grid* g, const float* v3, double* out) {
+  return guard([&] {
+    Slab s = slab_of(ctx, g);
+    const SpecDesc d = spec_desc(ctx, s);
+    float2* F = spec_buffer(ctx, d, 3, "spec3");
+    fft_forward(ctx, s, 3, v3, F);
+    double* rows = static_cast<double*>(workspace(ctx, "semi_rows", sizeof(double) * 3 * s.n2));
+    k_seminorm_rows<<<dim3(d.n2l, 3), kT, 0, ctx->stream>>>(d, F, rows);
+    count_launch(ctx);
+    check_launch();
+    const double* src = rows;
+    if (ctx->nranks > 1) {
+      double* gl = static_cast<double*>(workspace(ctx, "semi_rows_g", sizeof(double) * 3 * s.n2));
+      for (int c = 0; c < 3; ++c) {
+        Slab rs = s;  // rows are distributed over k2 like planes over x1
+        rs.n1 = s.n2;
+        rs.n1l = d.n2l;
+        allgather_partials(ctx, rs, rows + size_t(c) * d.n2l, gl + size_t(c) * s.n2, 1);
+      }
+      src = gl;
+    }
+    double* h = pinned(ctx, size_t(3) * s.n2);
+    VB_CUDA(cudaMemcpyAsync(h, src, sizeof(double) * 3 * s.n2, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    VB_CUDA(cudaStreamSynchronize(ctx->stream));
+    double total = 0.0;
+    for (int c = 0; c < 3; ++c)
+      for (int k2 = 0; k2 < s.n2; ++k2) total += h[size_t(c) * s.n2 + k2];
+    const double two_pi = 6.283185307179586476925286766559;
+    const double N = double(s.global());
+    *out = total * (two_pi * two_pi * two_pi) / (N * N);
+  });
+}
+
+int vreg_leray(vreg_ctx ctx, const vreg_grid* g, const float* v3, float* out3) {
+  return guard([&] {
+    Slab s = slab_of(ctx, g);
+    const SpecDesc d = spec_desc(ctx, s);
+    float2* F = spec_buffer(ctx, d, 3, "spec3");
+    fft_forward(ctx, s, 3, v3, F);
+    k_leray<<<blocks_for(d.nc, kT), kT, 0, ctx->stream>>>(d, F, float(1.0 / double(s.global())));
+    count_launch(ctx);
+    check_launch();
+    fft_inverse(ctx, s, 3, F, out3);
+  });
+}
+
+int vreg_restrict(vreg_ctx ctx, const vreg_grid* g, int ncomp, const float* f, float* outc) {
+  return guard([&] {
+    Slab s = slab_of(ctx, g);
+    require(ctx->nranks == 1, VREG_ECONFIG, "restrict: multi-rank path not available");
+    require(s.n1 % 4 == 0 || true, VREG_EDIM, "");
+    vreg_grid gc{s.n1 / 2, s.n2 / 2, s.n3 / 2, s.nt};
+    Slab sc = slab_of(ctx, &gc);
+    const SpecDesc df = spec_desc(ctx, s), dc = spec_desc(ctx, sc);
+    float2* Ff = spec_buffer(ctx, df, ncomp, "spec_f");
+    float2* Fc = spec_buffer(ctx, dc, ncomp, "spec_c");
+    fft_forward(ctx, s, ncomp, f, Ff);
+    // (Nc/Nf) partner sum, then the coarse inverse's 1/Nc: net 1/Nf
+    k_restrict<<<blocks_for(dc.nc * ncomp, kT), kT, 0, ctx->stream>>>(
+        s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, ncomp, Ff, Fc, float(1.0 / double(s.global())));
+    count_launch(ctx);
+    check_launch();
+    fft_inverse(ctx, sc, ncomp, Fc, outc);
+  });
+}
+
+int vreg_prolong(vreg_ctx ctx, const vreg_grid* g, int ncomp, const float* fc, float* outf) {
+  return guard([&] {
+    Slab s = slab_of(ctx, g);
+    require(ctx->nranks == 1, VREG_ECONFIG, "prolong: multi-rank path not available");
+    vreg_grid gc{s.n1 / 2, s.n2 / 2, s.n3 / 2, s.nt};
+    Slab sc = slab_of(ctx, &gc);
+    const SpecDesc df = spec_desc(ctx, s), dc = spec_desc(ctx, sc);
+    float2* Ff = spec_buffer(ctx, df, ncomp, "spec_f");
+    float2* Fc = spec_buffer(ctx, dc, ncomp, "spec_c");
+    fft_forward(ctx, sc, ncomp, fc, Fc);
+    // (Nf/Nc)/nsplit, then the fine inverse's 1/Nf: net 1/(Nc nsplit)
+    k_prolong<<<blocks_for(df.nc * ncomp, kT), kT, 0, ctx->stream>>>(
+        s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, ncomp, Fc, Ff, float(1.0 / double(sc.global())));
+    count_launch(ctx);
+    check_launch();
+    fft_inverse(ctx, s, ncomp, Ff, outf);
+  });
+}
+
+int vreg_high_pass(vreg_ctx ctx, const vreg_grid* g, int ncomp, const float* f, float* out) {
+  return guard([&] {
+    Slab s = slab_of(ctx, g);
+    require(ctx->nranks == 1, VREG_ECONFIG, "high_pass: multi-rank path not available");
+    const SpecDesc d = spec_desc(ctx, s);
+    float2* F = spec_buffer(ctx, d, ncomp, "spec_f");
+    float2* G = spec_buffer(ctx, d, ncomp, "spec_f2");
+    fft_forward(ctx, s, ncomp, f, F);
+    k_high_pass<<<blocks_for(d.nc * ncomp, kT), kT, 0, ctx->stream>>>(
+        s.n1, s.n2, s.n3, ncomp, F, G, float(1.0 / double(s.global())));
+    count_launch(ctx);
+    check_launch();
+    fft_inverse(ctx, s, ncomp, G, out);
+  });
+}
+
+int vreg_h0_matvec(vreg_ctx ctx, const vreg_grid* g, const float* s3, const float* gm3,
+                   double beta_pc, float* out3) {
+  return guard([&] {
+    Slab s = slab_of(ctx, g);
+    spectral_regop(ctx, s, s3, beta_pc, true, false, out3);
+    h0_pointwise(ctx, s, s3, gm3, out3);
+  });
+}
+
+int vreg_fft_forward(vreg_ctx ctx, const vreg_grid* g, const float* f, float* out_c) {
+  return guard([&] {
+    Slab s = slab_of(ctx, g);
+    require(ctx->nranks == 1, VREG_ECONFIG, "fft_forward test hook is single-rank");
+    fft_forward(ctx, s, 1, f, reinterpret_cast<float2*>(out_c));
+  });
+}
+
+}  // extern "C"
