@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark of the GN Hessian-matvec hot path (BASELINE.json north_star).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--n 256] [--degree 3]
+
+One step = one Gauss-Newton Hessian matvec (optim.hpp:115-137, Transpose
+adjoint, gradient cache on) at the SYN linearisation point v = 0.5 v_syn,
+vt = -g, nt = 4, cubic, beta = 1e-3, fp32 on device.
+N = 1: the 256^3 configuration (BASELINE.json configs[1]). N > 1: weak
+scaling at 256^3 voxels per GPU, slab-decomposed along x1
+(512x256x256 @2, 512x512x256 @4, 512^3 @8); --n 512 gives the 512^3-per-GPU
+family up to 1024^3 on 8 GPUs.
+
+Metric: matvec throughput in Mvox*matvec/s (grid points x matvecs / s),
+whole job. Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GN Hessian matvec throughput (SYN, nt=4, cubic, H1, beta=1e-3)"
+UNIT = "Mvox*matvec/s"
+BETA = 1e-3
+NT = 4
+
+
+def weak_grid(n, N):
+    """Per-GPU work fixed: double x1, then x2, then x3 (slab axis first)."""
+    dims = [n, n, n]
+    k, a = N, 0
+    while k > 1:
+        dims[a % 3] *= 2
+        k //= 2
+        a += 1
+    return tuple(dims)
+
+
+def bytes_per_voxel(nt):
+    """Algorithmic HBM bytes per grid point of our fused matvec:
+    inc-state init 28 + nt x 44, nt scatter sweeps x 28, assembly
+    16 (nt+1) + 24, spectral symbol pass 3 x 8.06."""
+    return 28 + 44 * nt + 28 * nt + 16 * (nt + 1) + 24 + 3 * 8.06
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        try:
+            with open(p) as f:
+                return float(json.load(f)["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    --set full summary (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------- CPU legs ----
+
+def cpu_reference_sample(n=128, matvecs=1):
+    """The UNMODIFIED reference (oracle/_ref, fp64, single-threaded: it has no
+    threading) on the host: `matvecs` GN matvecs at the SYN linearisation
+    point on an n^3 grid. Returns (Mvox*matvec/s, seconds, kind, sample)."""
+    import numpy as np
+    from oracle import ref
+    if ref.available():
+        m0, v, m1 = ref.syn(n, NT, 3)
+        s = ref.Session(m0, m1, 0.5 * v, BETA, ref.Config(continuation=False, beta_target=BETA))
+        vt = -s.gradient()
+        t0 = time.perf_counter()
+        for _ in range(matvecs):
+            s.matvec(vt)
+        dt = time.perf_counter() - t0
+        return n ** 3 * matvecs / dt / 1e6, dt, "reference", \
+            f"{matvecs} GN matvec(s) of the compiled reference at {n}^3 (fp64, 1 thread)"
+    from oracle import vreg_np as O
+    n = min(n, 64)
+    m0 = O.syn_template((n,) * 3)
+    v = O.syn_velocity((n,) * 3)
+    fwd, _ = O.characteristics(v, NT)
+    m1 = O.solve_state(fwd, m0, NT)[-1]
+    L = O.Linearization(m0, m1, 0.5 * v, BETA)
+    t0 = time.perf_counter()
+    for _ in range(matvecs):
+        L.matvec(-L.g)
+    dt = time.perf_counter() - t0
+    return n ** 3 * matvecs / dt / 1e6, dt, "port", \
+        f"{matvecs} GN matvec(s) of the numpy restatement at {n}^3 (fp64)"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = 128
+    vals = []
+    # warm-up steps are part of the contract; each step is one 128^3 matvec
+    from oracle import ref
+    import numpy as np
+    if ref.available():
+        m0, v, m1 = ref.syn(n, NT, 3)
+        s = ref.Session(m0, m1, 0.5 * v, BETA, ref.Config(continuation=False, beta_target=BETA))
+        vt = -s.gradient()
+        for _ in range(args.warmup):
+            s.matvec(vt)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            s.matvec(vt)
+        dt = time.perf_counter() - t0
+        kind, sample = "reference", f"{args.steps} GN matvecs of the compiled reference at {n}^3 (fp64, 1 thread; the reference has no threading)"
+    else:
+        val, dt, kind, sample = cpu_reference_sample(64, args.steps)
+        n = 64
+    value = n ** 3 * args.steps / dt / 1e6
+    nx, ny, nz = (args.n,) * 3 if args.gpus == 1 else weak_grid(args.n, args.gpus)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"SYN {nx}x{ny}x{nz} GN Hessian matvec (sample at {n}^3 on CPU)",
+                   "grid": [nx, ny, nz], "nt": NT, "interp_degree": 3, "beta": BETA},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU leg ----
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2008_12820_b200 import Context
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        obj = [Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = Context(local, rank, world, obj[0])
+    else:
+        ctx = Context(local)
+
+    dims = (args.n,) * 3 if world == 1 else weak_grid(args.n, world)
+    g = ctx.grid(*dims, nt=NT)
+    deg = args.degree
+    Nvox = dims[0] * dims[1] * dims[2]
+
+    # linearisation point, built on device (SYN inputs, syn.cpp:9-49)
+    m0 = ctx.syn_template(g)
+    vsyn = ctx.syn_velocity(g)
+    m1 = ctx.solve_state(g, ctx.characteristics(g, vsyn, deg), m0, deg)[NT].clone()
+    v = (0.5 * vsyn).contiguous()
+    del vsyn
+    fwd = ctx.characteristics(g, v, deg)
+    m = ctx.solve_state(g, fwd, m0, deg)
+    grads = torch.stack([ctx.fd_grad(g, m[t].contiguous()) for t in range(NT + 1)])
+    bwd = ctx.characteristics(g, (-v).contiguous(), deg)
+    q = ctx.adjoint_source_factor(g, v, bwd, deg)
+    lam = ctx.adjoint_sweep(g, bwd, q, (m1 - m[NT]).contiguous(), deg)
+    grad = ctx.integrate_lambda_grad_m(g, lam, grads)
+    ctx.axpy(g, 1.0, ctx.regop(g, v, BETA, False), grad)
+    vt = (-grad).contiguous()
+    del lam, q, bwd, m
+    out = torch.empty_like(vt)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        ctx.gn_matvec(g, fwd, grads, BETA, vt, deg, out=out)
+
+    for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
+        step()
+    barrier()
+
+    # ---- timed region: K matvecs, inputs resident in HBM (> L2: no flush needed)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launches()
+    ctx.enable_timers(True)
+    t_before = ctx.timers()
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = ctx.launches() - l0
+    ctx.enable_timers(False)
+    kstats = ctx.kernel_stats()
+    t_after = ctx.timers()
+
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = Nvox * args.steps / (ms * 1e-3) / 1e6
+
+    # ---- e2e: the public API with HOST buffers, copies inside the timed region
+    h_in = torch.empty(vt.shape, dtype=torch.float32, pin_memory=True)
+    h_in.copy_(vt)
+    h_out = torch.empty(vt.shape, dtype=torch.float32, pin_memory=True)
+    d_in = torch.empty_like(vt)
+
+    def step_e2e():
+        d_in.copy_(h_in, non_blocking=True)
+        ctx.gn_matvec(g, fwd, grads, BETA, d_in, deg, out=out)
+        h_out.copy_(out, non_blocking=True)
+
+    for _ in range(2):
+        step_e2e()
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step_e2e()
+    ev1.record(stream)
+    barrier()
+    ms_e2e = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_e2e = float(t.item())
+    e2e_value = Nvox * args.steps / (ms_e2e * 1e-3) / 1e6
+    nbytes = vt.numel() * 4
+
+    if rank == 0:
+        peak, peak_kind = measured_peak()
+        # dominant kernel by device time inside the timed region
+        dom = max(kstats.items(), key=lambda kv: kv[1]["seconds"]) if kstats else None
+        roof = None
+        if dom:
+            name, st = dom
+            per_launch_s = st["seconds"] / max(st["count"], 1)
+            Nloc = Nvox // world
+            bpv = {"sl_scatter_sweep": 28.0, "sl_inc_step": 44.0, "sl_assemble": 16.0 * (NT + 1) + 24.0,
+                   "sl_inc_init": 28.0}.get(name)
+            traffic = ncu_traffic()
+            roof = {"bound": "hbm", "kernel": name, "peak": peak, "peak_kind": peak_kind,
+                    "unit": "GB/s", "bytes_per_voxel": bpv,
+                    "launch_us": per_launch_s * 1e6, "launches": st["count"],
+                    "traffic": (traffic or {}).get(name)}
+            if bpv:
+                ach = bpv * Nloc / per_launch_s / 1e9
+                roof.update({"achieved": ach, "frac": ach / peak})
+        matvec_bytes = bytes_per_voxel(NT) * (Nvox // world)
+        share = {k: round(v["seconds"] / (ms * 1e-3) , 4) for k, v in kstats.items()}
+        fft_s = t_after["fft"] - t_before["fft"]
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            val, dt, kind, sample = cpu_reference_sample(128, 1)
+            cpu = {"value": val, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample,
+                   "seconds": dt, "host_cores": os.cpu_count()}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"SYN {dims[0]}x{dims[1]}x{dims[2]} GN Hessian matvec",
+                       "grid": list(dims), "nt": NT, "interp_degree": deg, "beta": BETA,
+                       "precond": None, "parallelism": f"x1-slab x{world}",
+                       "l2": "inputs > L2 (grads+chars+vt ~ %.1f GB/GPU)" % (
+                           (3 * (NT + 1) + 6) * 4 * Nvox / world / 1e9)},
+            "matvec_per_s": args.steps / (ms * 1e-3),
+            "matvec_gbs": matvec_bytes / (ms / args.steps * 1e-3) / 1e9,
+            "matvec_frac_of_hbm": matvec_bytes / (ms / args.steps * 1e-3) / 1e9 / peak,
+            "fft_ms_per_step": fft_s / args.steps * 1e3,
+            "kernel_share": share,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+                    "d2h_bytes_per_step": nbytes, "ms_per_step": ms_e2e / args.steps},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--degree", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

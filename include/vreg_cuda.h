@@ -71,6 +71,11 @@ int vreg_slab(vreg_ctx ctx, const vreg_grid* g, int* n1_local, int* offset);
  * transpose_comm (counters.hpp:69-78), seconds, measured with CUDA events. */
 int vreg_ctx_enable_timers(vreg_ctx ctx, int on);
 int vreg_ctx_timers(vreg_ctx ctx, double out8[8]);
+/* Per-kernel device time while timers are on: the idx-th named kernel
+ * (sorted by name); returns VREG_EPARAM past the end. */
+int vreg_ctx_kernel_stats(vreg_ctx ctx, int idx, char name64[64], uint64_t* count,
+                          double* seconds);
+int vreg_ctx_reset_kernel_stats(vreg_ctx ctx);
 /* Communication volume per category (counters.hpp:49-59), bytes. */
 int vreg_ctx_comm(vreg_ctx ctx, uint64_t out9[9]);
 /* Number of kernel launches issued by this library since creation. */

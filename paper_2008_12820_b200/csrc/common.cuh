@@ -132,8 +132,10 @@ struct vreg_ctx_s {
   bool timers_on = false;
   struct Pending {
     int cat;
+    const char* name;
     cudaEvent_t a, b;
   };
+  std::map<std::string, std::pair<uint64_t, double>> kstats;  // per named kernel
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
   double timer_acc[vb::T_COUNT] = {0};
@@ -157,13 +159,14 @@ struct Slab {
 Slab slab_of(vreg_ctx ctx, const vreg_grid* g);
 
 void* workspace(vreg_ctx ctx, const std::string& name, size_t bytes);
+void resolve_timers(vreg_ctx ctx);
 double* pinned(vreg_ctx ctx, size_t n);
 
 FftPlans& fft_plans(vreg_ctx ctx, int n1, int n2, int n3, int batch);
 
 class Timed {
  public:
-  Timed(vreg_ctx ctx, int cat);
+  Timed(vreg_ctx ctx, int cat, const char* name = nullptr);
   ~Timed();
   Timed(const Timed&) = delete;
   Timed& operator=(const Timed&) = delete;
@@ -171,6 +174,7 @@ class Timed {
  private:
   vreg_ctx ctx_;
   int cat_;
+  const char* name_;
   cudaEvent_t a_ = nullptr;
 };
 

@@ -1,7 +1,9 @@
 // Context lifecycle, pooled memory, workspace cache, FFT plan cache, kernel
 // timers and slab distribution (EngineState analogue, engine.hpp:14-19;
 // FftPlanCache, fft.cpp:66-72; from_global/to_global, engine.hpp:63-66).
+#include <cstdio>
 #include <cstring>
+#include <iterator>
 #include <mutex>
 
 #include "common.cuh"
@@ -95,7 +97,7 @@ FftPlans& fft_plans(vreg_ctx ctx, int n1, int n2, int n3, int batch) {
   return ctx->plans.emplace(key, p).first->second;
 }
 
-Timed::Timed(vreg_ctx ctx, int cat) : ctx_(ctx), cat_(cat) {
+Timed::Timed(vreg_ctx ctx, int cat, const char* name) : ctx_(ctx), cat_(cat), name_(name) {
   if (!ctx_->timers_on) return;
   if (ctx_->event_pool.empty()) {
     cudaEvent_t e;
@@ -117,7 +119,24 @@ Timed::~Timed() {
     ctx_->event_pool.pop_back();
   }
   cudaEventRecord(b, ctx_->stream);
-  ctx_->pending.push_back({cat_, a_, b});
+  ctx_->pending.push_back({cat_, name_, a_, b});
+}
+
+void resolve_timers(vreg_ctx ctx) {
+  VB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (auto& p : ctx->pending) {
+    float ms = 0.f;
+    VB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    ctx->timer_acc[p.cat] += double(ms) * 1e-3;
+    if (p.name) {
+      auto& st = ctx->kstats[p.name];
+      st.first += 1;
+      st.second += double(ms) * 1e-3;
+    }
+    ctx->event_pool.push_back(p.a);
+    ctx->event_pool.push_back(p.b);
+  }
+  ctx->pending.clear();
 }
 
 }  // namespace vb
@@ -251,16 +270,28 @@ int vreg_ctx_enable_timers(vreg_ctx ctx, int on) {
 
 int vreg_ctx_timers(vreg_ctx ctx, double out8[8]) {
   return guard([&] {
-    VB_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (auto& p : ctx->pending) {
-      float ms = 0.f;
-      VB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
-      ctx->timer_acc[p.cat] += double(ms) * 1e-3;
-      ctx->event_pool.push_back(p.a);
-      ctx->event_pool.push_back(p.b);
-    }
-    ctx->pending.clear();
+    resolve_timers(ctx);
     for (int i = 0; i < T_COUNT; ++i) out8[i] = ctx->timer_acc[i];
+  });
+}
+
+int vreg_ctx_kernel_stats(vreg_ctx ctx, int idx, char* name64, uint64_t* count,
+                          double* seconds) {
+  return guard([&] {
+    resolve_timers(ctx);
+    require(idx >= 0 && size_t(idx) < ctx->kstats.size(), VREG_EPARAM, "no such kernel stat");
+    auto it = ctx->kstats.begin();
+    std::advance(it, idx);
+    std::snprintf(name64, 64, "%s", it->first.c_str());
+    *count = it->second.first;
+    *seconds = it->second.second;
+  });
+}
+
+int vreg_ctx_reset_kernel_stats(vreg_ctx ctx) {
+  return guard([&] {
+    resolve_timers(ctx);
+    ctx->kstats.clear();
   });
 }
 

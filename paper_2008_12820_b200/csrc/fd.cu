@@ -198,7 +198,7 @@ int vreg_fd_grad(vreg_ctx ctx, const vreg_grid* gr, const float* f, float* out3)
       require(s.n1l >= H, VREG_ECONFIG, "slab width below the FD ghost width 4");
       gh = halo_exchange(ctx, s, f, H, "fd_ghost", T_GHOST, C_GHOST_FD);
     }
-    Timed t(ctx, T_FD);
+    Timed t(ctx, T_FD, "fd_grad");
     const FdGeo g = fd_geo(s);
     const dim3 grid((s.n3 + TX - 1) / TX, (s.n2 + TY - 1) / TY, s.n1l), block(TX, TY);
     const float h1 = float(1.0 / s.h(0)), h2 = float(1.0 / s.h(1)), h3 = float(1.0 / s.h(2));
@@ -223,7 +223,7 @@ int vreg_fd_div(vreg_ctx ctx, const vreg_grid* gr, const float* v3, float* out) 
       require(s.n1l >= H, VREG_ECONFIG, "slab width below the FD ghost width 4");
       gh = halo_exchange(ctx, s, v3, H, "fd_ghost", T_GHOST, C_GHOST_FD);
     }
-    Timed t(ctx, T_FD);
+    Timed t(ctx, T_FD, "fd_div");
     const FdGeo g = fd_geo(s);
     const dim3 grid((s.n3 + TX - 1) / TX, (s.n2 + TY - 1) / TY, s.n1l), block(TX, TY);
     const float h1 = float(1.0 / s.h(0)), h2 = float(1.0 / s.h(1)), h3 = float(1.0 / s.h(2));

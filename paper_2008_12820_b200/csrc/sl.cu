@@ -260,7 +260,7 @@ void interp_sweep(vreg_ctx ctx, const Slab& s, const float* f, const float* disp
   const bool dist = ctx->nranks > 1;
   Ghosts gh;
   if (dist) gh = halo_exchange(ctx, s, f, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
-  Timed t(ctx, T_SL);
+  Timed t(ctx, T_SL, "sl_interp");
   const Geo g = geo_of(s);
   const dim3 grid = sl_grid(s), block(BX, BY);
   if (q)
@@ -284,11 +284,11 @@ void scatter_sweep(vreg_ctx ctx, const Slab& s, const float* z, const float* dis
   }
   require(out != z, VREG_EPARAM, "scatter cannot run in place");
   const bool dist = ctx->nranks > 1;
-  VB_CUDA(cudaMemsetAsync(out, 0, s.local() * sizeof(float), ctx->stream));
   GhostAcc acc;
   if (dist) acc = ghost_accumulators(ctx, s, ci.G, "sl_gacc");
   {
-    Timed t(ctx, T_SL);
+    Timed t(ctx, T_SL, "sl_scatter_sweep");
+    VB_CUDA(cudaMemsetAsync(out, 0, s.local() * sizeof(float), ctx->stream));
     const Geo g = geo_of(s);
     const dim3 grid = sl_grid(s), block(BX, BY);
     SL_DISPATCH(degree, dist,
@@ -322,7 +322,7 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
   const float half = float(0.5 * s.dt());
   float* w = static_cast<float*>(workspace(ctx, "inc_w", 2 * N * sizeof(float)));
   {
-    Timed t(ctx, T_SL);
+    Timed t(ctx, T_SL, "sl_inc_init");
     k_inc_init<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, vt3, grads, half, w);
     count_launch(ctx);
     check_launch();
@@ -338,7 +338,7 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
     float* mo = mt_all ? mt_all + size_t(t + 1) * N : nullptr;
     Ghosts gh;
     if (dist) gh = halo_exchange(ctx, s, wt, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
-    Timed tm(ctx, T_SL);
+    Timed tm(ctx, T_SL, "sl_inc_step");
     SL_DISPATCH(degree, dist,
                 (k_inc_step<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
                     g, src_of<DIST>(wt, gh), disp3, ci.identity ? 1 : 0, vt3,
@@ -358,7 +358,7 @@ void sl_transpose_sweeps(vreg_ctx ctx, const Slab& s, const float* disp3, int fl
 
 void sl_assemble(vreg_ctx ctx, const Slab& s, int descending, const float* sl,
                  const float* grads, const float* reg, float* out3) {
-  Timed t(ctx, T_SL);
+  Timed t(ctx, T_SL, "sl_assemble");
   const size_t N = s.local();
   k_assemble<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, s.nt, float(s.dt()), descending,
                                                             sl, grads, reg, out3);
@@ -388,7 +388,7 @@ int sl_characteristics(vreg_ctx ctx, const Slab& s, const float* v3, int degree,
     g2 = halo_exchange(ctx, s, v3 + N, G, "chars_g2", T_INTERP_COMM, C_GHOST_INTERP);
     g3 = halo_exchange(ctx, s, v3 + 2 * N, G, "chars_g3", T_INTERP_COMM, C_GHOST_INTERP);
   }
-  Timed t(ctx, T_SL);
+  Timed t(ctx, T_SL, "sl_characteristics");
   const Geo g = geo_of(s);
   const dim3 grid = sl_grid(s), block(BX, BY);
   const float m1 = float(-dt / s.h(0)), m2 = float(-dt / s.h(1)), m3 = float(-dt / s.h(2));

@@ -268,7 +268,7 @@ float2* spec_buffer(vreg_ctx ctx, const SpecDesc& d, int ncomp, const char* name
 }
 
 void fft_forward(vreg_ctx ctx, const Slab& s, int ncomp, const float* f, float2* F) {
-  Timed t(ctx, T_FFT);
+  Timed t(ctx, T_FFT, "fft_r2c");
   if (ctx->nranks > 1) {
     dist_fft_forward(ctx, s, ncomp, f, F);
     return;
@@ -278,7 +278,7 @@ void fft_forward(vreg_ctx ctx, const Slab& s, int ncomp, const float* f, float2*
 }
 
 void fft_inverse(vreg_ctx ctx, const Slab& s, int ncomp, float2* F, float* f) {
-  Timed t(ctx, T_FFT);
+  Timed t(ctx, T_FFT, "fft_c2r");
   if (ctx->nranks > 1) {
     dist_fft_inverse(ctx, s, ncomp, F, f);
     return;
@@ -289,6 +289,7 @@ void fft_inverse(vreg_ctx ctx, const Slab& s, int ncomp, float2* F, float* f) {
 
 void apply_symbol(vreg_ctx ctx, const SpecDesc& d, int ncomp, float2* F, double beta, bool inverse,
                   bool unit_zero, double scale) {
+  Timed t(ctx, T_FFT, "spec_symbol");
   k_symbol<<<blocks_for(d.nc * ncomp, kT), kT, 0, ctx->stream>>>(
       d, ncomp, F, float(beta), inverse ? 1 : 0, unit_zero ? 1 : 0, float(scale));
   count_launch(ctx);

@@ -94,6 +94,18 @@ class Context:
                  "transpose_comm"]
         return dict(zip(names, list(out)))
 
+    def kernel_stats(self, reset=False):
+        """{name: {count, seconds}} of named kernels timed while timers were on."""
+        out, i = {}, 0
+        name = C.create_string_buffer(64)
+        cnt, sec = C.c_uint64(), C.c_double()
+        while lib().vreg_ctx_kernel_stats(self.h, i, name, C.byref(cnt), C.byref(sec)) == 0:
+            out[name.value.decode()] = {"count": cnt.value, "seconds": sec.value}
+            i += 1
+        if reset:
+            check(lib().vreg_ctx_reset_kernel_stats(self.h))
+        return out
+
     def comm(self):
         out = (C.c_uint64 * 9)()
         check(lib().vreg_ctx_comm(self.h, out))
