@@ -124,6 +124,16 @@ struct vreg_ctx_s {
   // named workspace buffers (reused across calls)
   std::map<std::string, std::pair<void*, size_t>> ws;
 
+  // per-characteristics tile box tables (sl_tile.cuh), small LRU
+  struct TileTable {
+    const float* disp;
+    int n1, n2, n3, n1l, deg;
+    int* table;
+    uint64_t used;
+  };
+  std::vector<TileTable> tile_tables;
+  uint64_t tile_clock = 0;
+
   // reduction scratch
   double* h_pinned = nullptr;  // host staging
   size_t h_pinned_cap = 0;

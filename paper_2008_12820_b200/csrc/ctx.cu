@@ -217,6 +217,7 @@ int vreg_ctx_destroy(vreg_ctx ctx) {
       cufftDestroy(kv.second.c2r);
     }
     for (auto& kv : ctx->ws) cudaFree(kv.second.first);
+    for (auto& t : ctx->tile_tables) cudaFree(t.table);
     if (ctx->fft_work) cudaFree(ctx->fft_work);
     if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
     for (auto& p : ctx->pending) {

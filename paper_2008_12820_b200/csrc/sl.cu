@@ -6,8 +6,13 @@
 // Thread mapping: CTA = 32 x3-columns x 8 x2-rows of one x1 plane, so a
 // warp's 32 departure points are contiguous nodes with near-identical
 // displacements and their 4x4x4 stencils overlap in L1.
+#include <cstdlib>
+#include <set>
+
 #include "common.cuh"
 #include "sl_common.cuh"
+#include "sl_quad.cuh"
+#include "sl_tile.cuh"
 
 namespace vb {
 
@@ -172,6 +177,282 @@ __global__ void __launch_bounds__(BX* BY) k_source_factor(Geo g, SrcField<DIST> 
   q[p] = (1.0f + half * dd) / (1.0f - half * dsrc.f[p]);
 }
 
+// ---- quad (4 x3-points per thread) variants, used when n3 % 4 == 0 --------
+
+#define SLQ_INDEX                                          \
+  const int k0 = 4 * (blockIdx.x * BX + threadIdx.x);      \
+  const int j = blockIdx.y * BY + threadIdx.y;             \
+  const int i = blockIdx.z;                                \
+  if (k0 >= g.n3 || j >= g.n2) return;                     \
+  const size_t p = (size_t(i) * g.n2 + j) * g.n3 + k0;
+
+__device__ __forceinline__ float4 ld4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+
+template <int DEG, bool DIST>
+__global__ void __launch_bounds__(BX* BY) k_interp_q(Geo g, SrcField<DIST> src,
+                                                     const float* __restrict__ D,
+                                                     const float* __restrict__ qf,
+                                                     float* __restrict__ out) {
+  SLQ_INDEX
+  Quad<DEG> Q;
+  Q.build(ld4(D + p), ld4(D + g.N + p), ld4(D + 2 * g.N + p));
+  float r[4];
+  quad_gather(g, src, Q, i, j, k0, r);
+  if (qf) {
+    const float4 m = ld4(qf + p);
+    r[0] *= m.x; r[1] *= m.y; r[2] *= m.z; r[3] *= m.w;
+  }
+  st4(out + p, r[0], r[1], r[2], r[3]);
+}
+
+template <int DEG, bool DIST>
+__global__ void __launch_bounds__(BX* BY) k_scatter_q(Geo g, DstField<DIST> dst,
+                                                      const float* __restrict__ D,
+                                                      const float* __restrict__ z) {
+  SLQ_INDEX
+  const float4 zz = ld4(z + p);
+  if (zz.x == 0.f && zz.y == 0.f && zz.z == 0.f && zz.w == 0.f) return;
+  const float zv[4] = {zz.x, zz.y, zz.z, zz.w};
+  Quad<DEG> Q;
+  Q.build(ld4(D + p), ld4(D + g.N + p), ld4(D + 2 * g.N + p));
+  quad_scatter(g, dst, Q, i, j, k0, zv);
+}
+
+template <int DEG, bool DIST>
+__global__ void __launch_bounds__(BX* BY) k_inc_step_q(Geo g, SrcField<DIST> wsrc,
+                                                       const float* __restrict__ D, int ident,
+                                                       const float* __restrict__ vt,
+                                                       const float* __restrict__ gr, float half,
+                                                       int last, float* __restrict__ w_next,
+                                                       float* __restrict__ mt_out) {
+  SLQ_INDEX
+  float G[4];
+  if (ident) {
+    const float4 w = ld4(wsrc.f + p);
+    G[0] = w.x; G[1] = w.y; G[2] = w.z; G[3] = w.w;
+  } else {
+    Quad<DEG> Q;
+    Q.build(ld4(D + p), ld4(D + g.N + p), ld4(D + 2 * g.N + p));
+    quad_gather(g, wsrc, Q, i, j, k0, G);
+  }
+  const float4 v1 = ld4(vt + p), v2 = ld4(vt + g.N + p), v3 = ld4(vt + 2 * g.N + p);
+  const float4 g1 = ld4(gr + p), g2 = ld4(gr + g.N + p), g3 = ld4(gr + 2 * g.N + p);
+  const float u[4] = {v1.x * g1.x + v2.x * g2.x + v3.x * g3.x, v1.y * g1.y + v2.y * g2.y + v3.y * g3.y,
+                      v1.z * g1.z + v2.z * g2.z + v3.z * g3.z, v1.w * g1.w + v2.w * g2.w + v3.w * g3.w};
+  float m[4], wn[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    m[q] = G[q] - half * u[q];
+    wn[q] = last ? -m[q] : m[q] - half * u[q];
+  }
+  if (mt_out) st4(mt_out + p, m[0], m[1], m[2], m[3]);
+  st4(w_next + p, wn[0], wn[1], wn[2], wn[3]);
+}
+
+// ---- tile-staged variants (sl_tile.cuh) -----------------------------------
+
+constexpr int kTileCap = BOX_CAP;
+
+template <int DEG, bool DIST>
+__device__ __forceinline__ float tile_gather(const Geo& g, const SrcField<DIST>& src,
+                                             const TileBox& b, bool fits, const float* fbox,
+                                             const float* __restrict__ D, int i, int j, int k,
+                                             size_t p) {
+  const float d1 = D[p], d2 = D[g.N + p], d3 = D[2 * g.N + p];
+  if (fits) {
+    BoxStencil<DEG> bs;
+    if (bs.build(b, i, j, k, d1, d2, d3)) return bs.gather(b, fbox);
+  }
+  return point_gather<DEG, DIST>(g, src, i, j, k, d1, d2, d3);
+}
+
+// Point `it` of this thread in the tile (warp w: rows it*8 + w; lanes: x3).
+#define TILE_PT(it)                                                          \
+  const int row_##it = (it) * (TILE_THREADS / 32) + (threadIdx.x >> 5);      \
+  const int i = blockIdx.z * TT1 + row_##it / TT2;                           \
+  const int j = blockIdx.y * TT2 + row_##it % TT2;                           \
+  const int k = blockIdx.x * TT3 + (threadIdx.x & 31);                       \
+  const bool ok = i < g.n1l && j < g.n2 && k < g.n3;                         \
+  const size_t p = ok ? (size_t(i) * g.n2 + j) * g.n3 + k : 0;
+
+// Gather kernels: issue the box as cp.async, prefetch the 8 points'
+// displacements meanwhile, then serve all taps from smem.
+template <int DEG, bool DIST, int MODE>  // MODE 0: interp(*q), 1: inc-state step
+__global__ void __launch_bounds__(TILE_THREADS, 3) k_gather_tile(
+    Geo g, SrcField<DIST> src, const int* __restrict__ boxes, const float* __restrict__ D,
+    const float* __restrict__ qf, float* __restrict__ out, const float* __restrict__ vt,
+    const float* __restrict__ gr, float half, int last, float* __restrict__ mt_out) {
+  extern __shared__ float fbox[];
+  const TileBox b = load_tile_box(boxes, tile_index());
+  const bool fits = b.ext[0] > 0;
+  if (fits) load_box(g, src, b, fbox);
+  float d1[TILE_PPT], d2[TILE_PPT], d3[TILE_PPT];
+#pragma unroll
+  for (int it = 0; it < TILE_PPT; ++it) {
+    TILE_PT(it)
+    d1[it] = ok ? D[p] : 0.f;
+    d2[it] = ok ? D[g.N + p] : 0.f;
+    d3[it] = ok ? D[2 * g.N + p] : 0.f;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < TILE_PPT; ++it) {
+    TILE_PT(it)
+    if (!ok) continue;
+    float G;
+    BoxStencil<DEG> bs;
+    if (fits && bs.build(b, i, j, k, d1[it], d2[it], d3[it]))
+      G = bs.gather(b, fbox);
+    else
+      G = point_gather<DEG, DIST>(g, src, i, j, k, d1[it], d2[it], d3[it]);
+    if constexpr (MODE == 0) {
+      out[p] = qf ? G * qf[p] : G;
+    } else {
+      const float u = vt[p] * gr[p] + vt[g.N + p] * gr[g.N + p] + vt[2 * g.N + p] * gr[2 * g.N + p];
+      const float m = G - half * u;
+      if (mt_out) mt_out[p] = m;
+      out[p] = last ? -m : m - half * u;
+    }
+  }
+}
+
+template <int DEG, bool DIST>
+__global__ void __launch_bounds__(TILE_THREADS, 3) k_scatter_tile(Geo g, DstField<DIST> dst,
+                                                                  const int* __restrict__ boxes,
+                                                                  const float* __restrict__ D,
+                                                                  const float* __restrict__ z) {
+  extern __shared__ int ibox[];
+  __shared__ unsigned s_zmax;
+  const TileBox b = load_tile_box(boxes, tile_index());
+  const bool fits = b.ext[0] > 0;
+  if (threadIdx.x == 0) s_zmax = 0u;
+  if (fits) {
+    const int words = b.ext[0] * b.ext[1] * BOX_PITCH;
+    for (int c = threadIdx.x; c < words; c += TILE_THREADS) ibox[c] = 0;
+  }
+  float zv[TILE_PPT], d1[TILE_PPT], d2[TILE_PPT], d3[TILE_PPT];
+  float zm = 0.f;
+#pragma unroll
+  for (int it = 0; it < TILE_PPT; ++it) {
+    TILE_PT(it)
+    zv[it] = ok ? z[p] : 0.f;
+    zm = fmaxf(zm, fabsf(zv[it]));
+    d1[it] = ok ? D[p] : 0.f;
+    d2[it] = ok ? D[g.N + p] : 0.f;
+    d3[it] = ok ? D[2 * g.N + p] : 0.f;
+  }
+  const unsigned zb = __reduce_max_sync(0xffffffffu, __float_as_uint(zm));
+  __syncthreads();  // s_zmax initialised, box zeroed
+  if ((threadIdx.x & 31) == 0) atomicMax(&s_zmax, zb);
+  __syncthreads();
+  zm = __uint_as_float(s_zmax);
+  if (zm == 0.0f) return;  // whole tile contributes nothing
+  int e = 0;
+  frexpf(zm, &e);  // max |z| < 2^e
+  const float S = ldexpf(1.0f, 27 - e), invS = ldexpf(1.0f, e - 27);
+#pragma unroll
+  for (int it = 0; it < TILE_PPT; ++it) {
+    TILE_PT(it)
+    if (!ok || zv[it] == 0.0f) continue;
+    BoxStencil<DEG> bs;
+    if (fits && bs.build(b, i, j, k, d1[it], d2[it], d3[it]))
+      bs.scatter(b, ibox, zv[it] * S);
+    else
+      point_scatter<DEG, DIST>(g, dst, i, j, k, d1[it], d2[it], d3[it], zv[it]);
+  }
+  if (fits) {
+    __syncthreads();
+    flush_box(g, dst, b, ibox, invS);
+  }
+}
+
+inline dim3 tile_grid(const Slab& s) {
+  return dim3(unsigned((s.n3 + TT3 - 1) / TT3), unsigned((s.n2 + TT2 - 1) / TT2),
+              unsigned((s.n1l + TT1 - 1) / TT1));
+}
+
+// Box table of the characteristics disp3 (cached per pointer/grid/degree;
+// `refresh` recomputes after the characteristics were rewritten). A stale
+// table only costs speed: points outside their box take the global path.
+const int* tile_table(vreg_ctx ctx, const Slab& s, const float* disp3, int degree, bool refresh) {
+  const Geo g = geo_of(s);
+  const dim3 grid = tile_grid(s);
+  auto build = [&](int* table) {
+    if (degree == 3)
+      k_tile_boxes<3><<<grid, TILE_THREADS, 0, ctx->stream>>>(g, disp3, table);
+    else
+      k_tile_boxes<1><<<grid, TILE_THREADS, 0, ctx->stream>>>(g, disp3, table);
+    count_launch(ctx);
+    check_launch();
+  };
+  for (auto& t : ctx->tile_tables) {
+    if (t.disp == disp3 && t.n1 == s.n1 && t.n2 == s.n2 && t.n3 == s.n3 && t.n1l == s.n1l &&
+        t.deg == degree) {
+      if (refresh) build(t.table);
+      t.used = ++ctx->tile_clock;
+      return t.table;
+    }
+  }
+  if (ctx->tile_tables.size() >= 16) {
+    auto lru = ctx->tile_tables.begin();
+    for (auto it = ctx->tile_tables.begin(); it != ctx->tile_tables.end(); ++it)
+      if (it->used < lru->used) lru = it;
+    VB_CUDA(cudaFreeAsync(lru->table, ctx->stream));
+    ctx->tile_tables.erase(lru);
+  }
+  const size_t ntiles = size_t(grid.x) * grid.y * grid.z;
+  int* table = nullptr;
+  VB_CUDA(cudaMallocAsync(&table, 6 * ntiles * sizeof(int), ctx->stream));
+  build(table);
+  ctx->tile_tables.push_back({disp3, s.n1, s.n2, s.n3, s.n1l, degree, table, ++ctx->tile_clock});
+  return table;
+}
+
+constexpr size_t kTileSmem = kTileCap * sizeof(float);
+
+// Opt a tile kernel in to kTileSmem of dynamic shared memory (once).
+template <class Kern>
+inline Kern tile_kernel(Kern k) {
+  static std::set<const void*> done;  // per kernel (same-signature kernels share Kern)
+  const void* key = reinterpret_cast<const void*>(k);
+  if (!done.count(key)) {
+    VB_CUDA(cudaFuncSetAttribute(key, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kTileSmem)));
+    done.insert(key);
+  }
+  return k;
+}
+
+// Tile kernels opt in to 48 KB of dynamic shared memory (VREG_SL_TILE=0
+// selects the per-point kernels, for A/B measurements).
+inline bool use_tile() {
+  static const bool on = [] {
+    const char* e = std::getenv("VREG_SL_TILE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+inline dim3 slq_grid(const Slab& s) {
+  return dim3(unsigned((s.n3 / 4 + BX - 1) / BX), unsigned((s.n2 + BY - 1) / BY), unsigned(s.n1l));
+}
+
+// Quad kernels (register-blocked, L1/L2 direct) need 16-byte aligned rows;
+// experimental, opt in with VREG_SL_QUAD=1 (and VREG_SL_TILE=0).
+inline bool use_quad(const Slab& s) {
+  static const bool on = [] {
+    const char* e = std::getenv("VREG_SL_QUAD");
+    return e && e[0] == '1';
+  }();
+  return on && s.n3 % 4 == 0;
+}
+
 template <bool DIST>
 SrcField<DIST> src_of(const float* f, const Ghosts& gh) {
   SrcField<DIST> s;
@@ -263,7 +544,19 @@ void interp_sweep(vreg_ctx ctx, const Slab& s, const float* f, const float* disp
   Timed t(ctx, T_SL, "sl_interp");
   const Geo g = geo_of(s);
   const dim3 grid = sl_grid(s), block(BX, BY);
-  if (q)
+  if (use_tile()) {
+    const int* boxes = tile_table(ctx, s, disp3, degree, false);
+    SL_DISPATCH(degree, dist,
+                (tile_kernel(k_gather_tile<DEG, DIST, 0>)<<<tile_grid(s), TILE_THREADS,
+                                                             kTileSmem, ctx->stream>>>(
+                    g, src_of<DIST>(f, gh), boxes, disp3, q, out, nullptr, nullptr, 0.f, 0,
+                    nullptr)));
+  }
+  else if (use_quad(s))
+    SL_DISPATCH(degree, dist,
+                (k_interp_q<DEG, DIST><<<slq_grid(s), block, 0, ctx->stream>>>(
+                    g, src_of<DIST>(f, gh), disp3, q, out)));
+  else if (q)
     SL_DISPATCH(degree, dist,
                 (k_interp_mul<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
                     g, src_of<DIST>(f, gh), disp3, q, out)));
@@ -291,9 +584,21 @@ void scatter_sweep(vreg_ctx ctx, const Slab& s, const float* z, const float* dis
     VB_CUDA(cudaMemsetAsync(out, 0, s.local() * sizeof(float), ctx->stream));
     const Geo g = geo_of(s);
     const dim3 grid = sl_grid(s), block(BX, BY);
-    SL_DISPATCH(degree, dist,
-                (k_scatter<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
-                    g, dst_of<DIST>(out, acc), disp3, z)));
+    if (use_tile()) {
+      const int* boxes = tile_table(ctx, s, disp3, degree, false);
+      SL_DISPATCH(degree, dist,
+                  (tile_kernel(k_scatter_tile<DEG, DIST>)<<<tile_grid(s), TILE_THREADS, kTileSmem,
+                                               ctx->stream>>>(g, dst_of<DIST>(out, acc), boxes,
+                                                              disp3, z)));
+    }
+    else if (use_quad(s))
+      SL_DISPATCH(degree, dist,
+                  (k_scatter_q<DEG, DIST><<<slq_grid(s), block, 0, ctx->stream>>>(
+                      g, dst_of<DIST>(out, acc), disp3, z)));
+    else
+      SL_DISPATCH(degree, dist,
+                  (k_scatter<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
+                      g, dst_of<DIST>(out, acc), disp3, z)));
   }
   if (dist) halo_reverse_add(ctx, s, acc, out, "sl_gacc");
 }
@@ -339,6 +644,20 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
     Ghosts gh;
     if (dist) gh = halo_exchange(ctx, s, wt, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
     Timed tm(ctx, T_SL, "sl_inc_step");
+    if (use_tile() && !ci.identity) {
+      const int* boxes = tile_table(ctx, s, disp3, degree, false);
+      SL_DISPATCH(degree, dist,
+                  (tile_kernel(k_gather_tile<DEG, DIST, 1>)<<<tile_grid(s), TILE_THREADS,
+                                                               kTileSmem, ctx->stream>>>(
+                      g, src_of<DIST>(wt, gh), boxes, disp3, nullptr, wn, vt3,
+                      grads + size_t(t + 1) * 3 * N, half, last ? 1 : 0, mo)));
+    }
+    else if (use_quad(s))
+      SL_DISPATCH(degree, dist,
+                  (k_inc_step_q<DEG, DIST><<<slq_grid(s), block, 0, ctx->stream>>>(
+                      g, src_of<DIST>(wt, gh), disp3, ci.identity ? 1 : 0, vt3,
+                      grads + size_t(t + 1) * 3 * N, half, last ? 1 : 0, wn, mo)));
+    else
     SL_DISPATCH(degree, dist,
                 (k_inc_step<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
                     g, src_of<DIST>(wt, gh), disp3, ci.identity ? 1 : 0, vt3,
@@ -428,6 +747,7 @@ int vreg_characteristics(vreg_ctx ctx, const vreg_grid* g, const float* v3, int 
   return guard([&] {
     Slab s = slab_of(ctx, g);
     int ident = sl_characteristics(ctx, s, v3, degree, disp3);
+    if (!ident && use_tile()) tile_table(ctx, s, disp3, degree, true);
     int flags = ident;
     if (ctx->nranks > 1 && !ident) flags |= (sl_ghost_width(ctx, s, disp3, degree) + 1) << 8;
     if (identity) *identity = flags;

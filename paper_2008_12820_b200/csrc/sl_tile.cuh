@@ -1,0 +1,272 @@
+// Tile-staged semi-Lagrangian sweeps (the hot kernels of the GN matvec).
+//
+// A CTA owns a 4 x 16 x 32 (x1, x2, x3) tile of departure points. Each tile
+// has a BOX of grid cells its stencils touch,
+//   box_a = [tile_a + min_a + O0, tile_a + T_a - 1 + max_a + O0 + NN - 1],
+// min/max over the tile of floor(disp_a). Boxes depend only on the
+// characteristics, so they are computed once per characteristics
+// (k_tile_boxes) and cached; ~2.8 cells per point for smooth flows.
+//
+// gather : the source box is loaded once (coalesced rows, periodic wrap /
+//          x1 ghost planes applied on load) into shared memory and every
+//          point's 64 taps are served from smem.
+// scatter: contributions accumulate in a shared-memory box in 32-bit fixed
+//          point (native ATOMS.ADD; fp32 smem atomics are a CAS loop on
+//          sm_100a, ~4x slower, tools/smem_atomic_bench.cu) with a per-tile
+//          power-of-two scale S = 2^(27-e), max|z_tile| < 2^e, so each
+//          contribution is exact to 2^-28 max|z| and a cell absorbs > 8
+//          max|z| without overflow. The box is flushed once with fp32 REDs:
+//          ~3 L2 reductions per point instead of 64 (the L2 RED path is
+//          payload-bound at ~6.4 TB/s, tools/red_bench.cu).
+// Smem rows have a pitch of 64 words, so lanes of a warp (32 consecutive x3
+// points) whose x1/x2 offsets differ by one row/plane still hit distinct
+// banks. Tiles whose box exceeds the smem budget, and single points outside
+// a (stale) cached box, take the per-point global-memory path.
+#pragma once
+
+#include "sl_common.cuh"
+
+namespace vb {
+
+constexpr int TT1 = 4, TT2 = 16, TT3 = 32;
+constexpr int TILE_THREADS = 256;
+constexpr int TILE_POINTS = TT1 * TT2 * TT3;
+constexpr int TILE_PPT = TILE_POINTS / TILE_THREADS;  // points per thread (8)
+constexpr int BOX_PITCH = 64;                          // smem row pitch (words)
+constexpr int BOX_CAP = 16384;                         // smem words per CTA (64 KB)
+
+// Cached per-tile box: lo1, lo2, lo3, e1, e2, e3 (e1 = 0: empty, e1 < 0: no fit)
+struct TileBox {
+  int lo[3];
+  int ext[3];
+};
+
+__device__ __forceinline__ TileBox load_tile_box(const int* __restrict__ table, int tile) {
+  TileBox b;
+  const int* t = table + 6 * size_t(tile);
+  b.lo[0] = __ldg(t);
+  b.lo[1] = __ldg(t + 1);
+  b.lo[2] = __ldg(t + 2);
+  b.ext[0] = __ldg(t + 3);
+  b.ext[1] = __ldg(t + 4);
+  b.ext[2] = __ldg(t + 5);
+  return b;
+}
+
+__device__ __forceinline__ int tile_index() {
+  return (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+}
+
+// Point (i, j, k) of iteration `it` of this thread: warp w covers rows
+// (x1, x2) = (it*8 + w) / TT2, % TT2 and its lanes the 32 x3 columns.
+#define TILE_POINT_LOOP(g)                                                     \
+  const int t1 = blockIdx.z * TT1, t2 = blockIdx.y * TT2, t3 = blockIdx.x * TT3; \
+  const int k = t3 + (threadIdx.x & 31);                                       \
+  _Pragma("unroll 1") for (int it = 0; it < TILE_PPT; ++it) {                  \
+    const int row = it * (TILE_THREADS / 32) + (threadIdx.x >> 5);             \
+    const int i = t1 + row / TT2, j = t2 + row % TT2;                          \
+    if (i >= (g).n1l || j >= (g).n2 || k >= (g).n3) continue;                  \
+    const size_t p = (size_t(i) * (g).n2 + j) * (g).n3 + k;
+
+#define TILE_POINT_LOOP_END }
+
+// ---- box computation (one CTA per tile) ------------------------------------
+
+template <int DEG>
+__global__ void __launch_bounds__(TILE_THREADS) k_tile_boxes(Geo g, const float* __restrict__ D,
+                                                             int* __restrict__ table) {
+  constexpr int NN = DEG + 1, O0 = DEG == 3 ? -1 : 0;
+  __shared__ int smn[3], smx[3];
+  if (threadIdx.x < 3) {
+    smn[threadIdx.x] = 1 << 30;
+    smx[threadIdx.x] = -(1 << 30);
+  }
+  __syncthreads();
+  int mn[3] = {1 << 30, 1 << 30, 1 << 30}, mx[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
+  TILE_POINT_LOOP(g)
+  const int f[3] = {int(floorf(D[p])), int(floorf(D[g.N + p])), int(floorf(D[2 * g.N + p]))};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    mn[a] = min(mn[a], f[a]);
+    mx[a] = max(mx[a], f[a]);
+  }
+  TILE_POINT_LOOP_END
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    mn[a] = __reduce_min_sync(0xffffffffu, mn[a]);
+    mx[a] = __reduce_max_sync(0xffffffffu, mx[a]);
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&smn[a], mn[a]);
+      atomicMax(&smx[a], mx[a]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int t[3] = {int(blockIdx.z) * TT1, int(blockIdx.y) * TT2, int(blockIdx.x) * TT3};
+    const int T[3] = {min(TT1, g.n1l - t[0]), min(TT2, g.n2 - t[1]), min(TT3, g.n3 - t[2])};
+    int* out = table + 6 * size_t(tile_index());
+    int e[3];
+    for (int a = 0; a < 3; ++a) {
+      out[a] = t[a] + smn[a] + O0;
+      e[a] = T[a] - 1 + (smx[a] - smn[a]) + NN;
+    }
+    // single-period wrap on load/flush needs every box coordinate in [-n, 2n)
+    const int n[3] = {g.n1, g.n2, g.n3};
+    bool fits = e[2] <= BOX_PITCH && e[0] * e[1] * BOX_PITCH <= BOX_CAP;
+    for (int a = 0; a < 3; ++a) fits = fits && e[a] <= n[a] && out[a] >= -n[a] && out[a] + e[a] <= 2 * n[a];
+    out[3] = fits ? e[0] : -1;
+    out[4] = e[1];
+    out[5] = e[2];
+  }
+}
+
+// ---- smem box I/O ----------------------------------------------------------
+// Warps walk box rows (u1 outer, u2 strided by warp), lanes the columns. Box
+// coordinates stay within one period of the grid (ext < n), so periodic wrap
+// is a single conditional add/subtract -- no integer division anywhere.
+
+__device__ __forceinline__ int wrap_once(int x, int n) {
+  return x < 0 ? x + n : (x >= n ? x - n : x);
+}
+
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Issue the box load as cp.async (LDGSTS: no register staging); the caller
+// overlaps its own global loads and then calls cp_async_wait_all() +
+// __syncthreads().
+template <bool DIST>
+__device__ __forceinline__ void load_box(const Geo& g, const SrcField<DIST>& src,
+                                         const TileBox& b, float* sbox) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int c0 = wrap_once(b.lo[2] + lane, g.n3);
+  int c1 = wrap_once(b.lo[2] + lane + 32, g.n3);
+  for (int u1 = 0; u1 < b.ext[0]; ++u1) {
+    int p1 = b.lo[0] + u1;
+    if constexpr (!DIST) p1 = wrap_once(p1, g.n1);
+    const float* P = src.plane_ptr(p1, g);
+    float* SP = sbox + u1 * b.ext[1] * BOX_PITCH;
+    for (int u2 = warp; u2 < b.ext[1]; u2 += TILE_THREADS / 32) {
+      const float* R = P + size_t(wrap_once(b.lo[1] + u2, g.n2)) * g.n3;
+      float* S = SP + u2 * BOX_PITCH;
+      if (lane < b.ext[2]) cp_async4(S + lane, R + c0);
+      if (lane + 32 < b.ext[2]) cp_async4(S + lane + 32, R + c1);
+    }
+  }
+}
+
+template <bool DIST>
+__device__ __forceinline__ void flush_box(const Geo& g, const DstField<DIST>& dst,
+                                          const TileBox& b, const int* sbox, float invS) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int c0 = wrap_once(b.lo[2] + lane, g.n3);
+  int c1 = wrap_once(b.lo[2] + lane + 32, g.n3);
+  for (int u1 = 0; u1 < b.ext[0]; ++u1) {
+    int p1 = b.lo[0] + u1;
+    if constexpr (!DIST) p1 = wrap_once(p1, g.n1);
+    float* P = dst.plane_ptr(p1, g);
+    const int* SP = sbox + u1 * b.ext[1] * BOX_PITCH;
+    for (int u2 = warp; u2 < b.ext[1]; u2 += TILE_THREADS / 32) {
+      float* R = P + size_t(wrap_once(b.lo[1] + u2, g.n2)) * g.n3;
+      const int* S = SP + u2 * BOX_PITCH;
+      if (lane < b.ext[2]) {
+        const int v = S[lane];
+        if (v != 0) atomicAdd(R + c0, float(v) * invS);
+      }
+      if (lane + 32 < b.ext[2]) {
+        const int v = S[lane + 32];
+        if (v != 0) atomicAdd(R + c1, float(v) * invS);
+      }
+    }
+  }
+}
+
+// ---- per-point stencil in box coordinates ---------------------------------
+
+template <int DEG>
+struct BoxStencil {
+  static constexpr int NN = DEG + 1, O0 = DEG == 3 ? -1 : 0;
+  int base;  // smem word index of tap (0,0,0)
+  float w1[NN], w2[NN], w3[NN];
+
+  // false if the stencil leaves the box (stale cache) -> caller falls back
+  __device__ __forceinline__ bool build(const TileBox& b, int i, int j, int k, float d1, float d2,
+                                        float d3) {
+    int b1, b2, b3;
+    float s1, s2, s3;
+    split_axis(d1, i, b1, s1);
+    split_axis(d2, j, b2, s2);
+    split_axis(d3, k, b3, s3);
+    const int r1 = b1 + O0 - b.lo[0], r2 = b2 + O0 - b.lo[1], r3 = b3 + O0 - b.lo[2];
+    const bool in = (unsigned)r1 <= unsigned(b.ext[0] - NN) &&
+                    (unsigned)r2 <= unsigned(b.ext[1] - NN) &&
+                    (unsigned)r3 <= unsigned(b.ext[2] - NN);
+    lagrange_weights<DEG>(s1, w1);
+    lagrange_weights<DEG>(s2, w2);
+    lagrange_weights<DEG>(s3, w3);
+    base = (r1 * b.ext[1] + r2) * BOX_PITCH + r3;
+    return in;
+  }
+
+  __device__ __forceinline__ float gather(const TileBox& b, const float* sbox) const {
+    const int e23 = b.ext[1] * BOX_PITCH;
+    float acc1 = 0.f;
+#pragma unroll
+    for (int a = 0; a < NN; ++a) {
+      float acc2 = 0.f;
+#pragma unroll
+      for (int bb = 0; bb < NN; ++bb) {
+        const float* R = sbox + base + a * e23 + bb * BOX_PITCH;
+        float acc3 = 0.f;
+#pragma unroll
+        for (int c = 0; c < NN; ++c) acc3 += w3[c] * R[c];
+        acc2 += w2[bb] * acc3;
+      }
+      acc1 += w1[a] * acc2;
+    }
+    return acc1;
+  }
+
+  __device__ __forceinline__ void scatter(const TileBox& b, int* sbox, float zS) const {
+    const int e23 = b.ext[1] * BOX_PITCH;
+#pragma unroll
+    for (int a = 0; a < NN; ++a) {
+      const float za = w1[a] * zS;
+#pragma unroll
+      for (int bb = 0; bb < NN; ++bb) {
+        int* R = sbox + base + a * e23 + bb * BOX_PITCH;
+        const float zab = za * w2[bb];
+#pragma unroll
+        for (int c = 0; c < NN; ++c) atomicAdd(R + c, __float2int_rn(zab * w3[c]));
+      }
+    }
+  }
+};
+
+// ---- per-point global fallbacks (rare; kept out of line) -------------------
+
+template <int DEG, bool DIST>
+__device__ __noinline__ float point_gather(const Geo& g, const SrcField<DIST> src, int i, int j,
+                                           int k, float d1, float d2, float d3) {
+  Stencil<DEG> st;
+  st.template build<DIST>(g, i, j, k, d1, d2, d3);
+  return st.gather(g, src);
+}
+
+template <int DEG, bool DIST>
+__device__ __noinline__ void point_scatter(const Geo& g, const DstField<DIST> dst, int i, int j,
+                                           int k, float d1, float d2, float d3, float z) {
+  Stencil<DEG> st;
+  st.template build<DIST>(g, i, j, k, d1, d2, d3);
+  st.scatter(g, dst, z);
+}
+
+}  // namespace vb
