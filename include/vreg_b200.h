@@ -1,0 +1,77 @@
+/* vreg_b200.h -- solver-level C ABI of libvreg_b200.so: the Gauss-Newton
+ * hot path behind a handle, for FFI callers (Python ctypes, bench, tests).
+ *
+ * Each entry point is the device counterpart of one reference call path
+ * (paths under /root/reference/proj):
+ *   vreg_solver_linearize  -> gauss_newton_level's setup: Flow + StateCache,
+ *                             evaluate_objective_with / evaluate_gradient_with
+ *                             (include/vreg/optim.hpp:155-168, 68-111)
+ *   vreg_solver_matvec     -> detail::hessian_matvec_with (optim.hpp:115-137)
+ *   vreg_solver_precond    -> Preconditioner<E>::refresh + apply
+ *                             (include/vreg/precond.hpp:80-162)
+ *   vreg_solver_register   -> register_images (optim.hpp:308-347)
+ * Field pointers are DEVICE pointers (this rank's x1 slab, fp32, vector
+ * fields as 3 consecutive components) unless the name says _host. Status
+ * codes as in vreg_cuda.h.
+ */
+#ifndef VREG_B200_H
+#define VREG_B200_H
+#include <stdint.h>
+
+#include "vreg_cuda.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* RegistrationConfig (optim.hpp:16-37); precond 0 InvA, 1 InvH0,
+ * 2 TwoLevelInvH0; hessian_adjoint 0 Transpose, 1 SemiLagrangian. */
+typedef struct {
+  double beta_target, beta_start;
+  int continuation;
+  double gamma_div;
+  int project_divfree;
+  double eps_newton, eps_h0;
+  int max_gn, max_pcg;
+  int precond;
+  int interp_degree;
+  int cache_state_gradient;
+  int fixed_gn, fixed_pcg;
+  int hessian_adjoint;
+  int nt;
+  double armijo_c, armijo_shrink;
+  int armijo_max_trials, h0_inner_cap;
+} vreg_config;
+
+typedef struct vreg_solver_s* vreg_solver;
+
+void vreg_config_default(vreg_config* cfg);
+int vreg_solver_create(vreg_ctx ctx, const vreg_grid* g, const vreg_config* cfg, vreg_solver* out);
+int vreg_solver_destroy(vreg_solver s);
+/* template m0 / reference m1 (device, local slab) */
+int vreg_solver_set_images(vreg_solver s, const float* m0, const float* m1);
+/* SYN pair built on device: m0 = syn_template, m1 = state of syn_velocity
+ * at t = 1 (proj/src/syn.cpp:46-49) */
+int vreg_solver_syn_images(vreg_solver s);
+int vreg_solver_images(vreg_solver s, float* m0, float* m1);
+/* linearisation point v (device vector field) at regularisation beta */
+int vreg_solver_linearize(vreg_solver s, const float* v3, double beta);
+int vreg_solver_objective(vreg_solver s, double J4[4]);
+int vreg_solver_gradient(vreg_solver s, float* g3);
+int vreg_solver_matvec(vreg_solver s, const float* vt3, float* out3);
+/* the same matvec on HOST buffers (H2D + matvec + D2H) */
+int vreg_solver_matvec_host(vreg_solver s, const float* vt3_host, float* out3_host);
+/* stats4: inva applications, h0 applications, inner iterations, capped */
+int vreg_solver_precond(vreg_solver s, int kind, const float* r3, double eps_k, float* out3,
+                        uint64_t stats4[4]);
+/* full solve from v = 0; rep16: initial_mismatch, final_mismatch, mism_rel,
+ * final_g_rel, total_gn, total_pcg, flagged, phases pc/obj/grad/hess/total,
+ * kernels fft/fd/sl, levels. counters21 in KernelCounters order. */
+int vreg_solver_register(vreg_solver s, float* v_out3, double rep16[16], uint64_t counters21[21]);
+int vreg_solver_counters(vreg_solver s, uint64_t counters21[21]);
+int vreg_solver_reset_counters(vreg_solver s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

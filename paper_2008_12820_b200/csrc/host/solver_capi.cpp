@@ -1,0 +1,301 @@
+// Solver-level C ABI (include/vreg_b200.h) over the C++ host layer
+// (include/vreg_b200/solver.hpp). Exceptions never cross the ABI: they map
+// back to the status codes of vreg_cuda.h.
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <string>
+
+#include "vreg_b200.h"
+#include "vreg_b200/solver.hpp"
+
+namespace vb {
+void set_last_error(const std::string& m);
+}
+
+using namespace vreg_b200;
+
+struct vreg_solver_s {
+  std::shared_ptr<Device> dev;
+  CudaEngine eng;
+  RegistrationConfig cfg;
+  DField m0, m1;
+  std::unique_ptr<Transport> lin;
+  ObjectiveValue J;
+  std::optional<DVField> grad;
+  Real beta = 0;
+  std::unique_ptr<Preconditioner> prec;
+};
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return VREG_OK;
+  } catch (const parameter_error& e) {
+    vb::set_last_error(e.what());
+    return VREG_EPARAM;
+  } catch (const numerical_error& e) {
+    vb::set_last_error(e.what());
+    return VREG_ENUMERICAL;
+  } catch (const io_error& e) {
+    vb::set_last_error(e.what());
+    return VREG_EIO;
+  } catch (const input_error& e) {
+    vb::set_last_error(e.what());
+    return VREG_EINPUT;
+  } catch (const dimension_error& e) {
+    vb::set_last_error(e.what());
+    return VREG_EDIM;
+  } catch (const config_error& e) {
+    vb::set_last_error(e.what());
+    return VREG_ECONFIG;
+  } catch (const std::exception& e) {
+    vb::set_last_error(e.what());
+    return VREG_ECUDA;
+  }
+}
+
+RegistrationConfig from_c(const vreg_config* c) {
+  RegistrationConfig r;
+  if (!c) return r;
+  r.beta_target = c->beta_target;
+  r.beta_start = c->beta_start;
+  r.continuation = c->continuation != 0;
+  r.gamma_div = c->gamma_div;
+  r.project_divfree = c->project_divfree != 0;
+  r.eps_newton = c->eps_newton;
+  r.eps_h0 = c->eps_h0;
+  r.max_gn = c->max_gn;
+  r.max_pcg = c->max_pcg;
+  r.precond = PrecondKind(c->precond);
+  r.interp_degree = c->interp_degree;
+  r.cache_state_gradient = c->cache_state_gradient != 0;
+  r.fixed_gn = c->fixed_gn;
+  r.fixed_pcg = c->fixed_pcg;
+  r.hessian_adjoint = HessianAdjoint(c->hessian_adjoint);
+  r.nt = c->nt;
+  r.armijo_c = c->armijo_c;
+  r.armijo_shrink = c->armijo_shrink;
+  r.armijo_max_trials = c->armijo_max_trials;
+  r.h0_inner_cap = c->h0_inner_cap;
+  return r;
+}
+
+void dump_counters(const KernelCounters& k, uint64_t* o) {
+  const uint64_t v[] = {k.fft_forward, k.fft_inverse, k.fft_forward_coarse, k.fft_inverse_coarse,
+                        k.fd_gradient, k.fd_divergence, k.ip_eval, k.ip_scatter,
+                        k.characteristics, k.characteristics_identity, k.sl_state, k.sl_adjoint,
+                        k.sl_inc_state, k.sl_inc_adjoint, k.pc_inva_apply, k.pc_h0_apply,
+                        k.pc_h0_inner_iters, k.pc_h0_inner_solves, k.pc_refresh,
+                        k.h0_inner_work_fine, k.h0_inner_work_coarse};
+  std::memcpy(o, v, sizeof(v));
+}
+
+void require_lin(const vreg_solver_s* s) {
+  if (!s->lin) throw config_error("solver not linearised (call vreg_solver_linearize)");
+}
+
+}  // namespace
+
+extern "C" {
+
+void vreg_config_default(vreg_config* c) {
+  RegistrationConfig r;
+  c->beta_target = r.beta_target;
+  c->beta_start = r.beta_start;
+  c->continuation = r.continuation;
+  c->gamma_div = r.gamma_div;
+  c->project_divfree = r.project_divfree;
+  c->eps_newton = r.eps_newton;
+  c->eps_h0 = r.eps_h0;
+  c->max_gn = r.max_gn;
+  c->max_pcg = r.max_pcg;
+  c->precond = int(r.precond);
+  c->interp_degree = r.interp_degree;
+  c->cache_state_gradient = r.cache_state_gradient;
+  c->fixed_gn = r.fixed_gn;
+  c->fixed_pcg = r.fixed_pcg;
+  c->hessian_adjoint = int(r.hessian_adjoint);
+  c->nt = r.nt;
+  c->armijo_c = r.armijo_c;
+  c->armijo_shrink = r.armijo_shrink;
+  c->armijo_max_trials = r.armijo_max_trials;
+  c->h0_inner_cap = r.h0_inner_cap;
+}
+
+int vreg_solver_create(vreg_ctx ctx, const vreg_grid* g, const vreg_config* cfg,
+                       vreg_solver* out) {
+  return guarded([&] {
+    if (!ctx || !g || !out) throw parameter_error("null argument");
+    auto s = std::make_unique<vreg_solver_s>();
+    s->cfg = from_c(cfg);
+    s->cfg.validate();
+    s->dev = Device::adopt(ctx);
+    Grid3 grid = Grid3::make(g->n1, g->n2, g->n3, s->cfg.nt);
+    s->eng = CudaEngine::create(grid, s->dev);
+    s->m0 = s->eng.make_field();
+    s->m1 = s->eng.make_field();
+    *out = s.release();
+  });
+}
+
+int vreg_solver_destroy(vreg_solver s) {
+  return guarded([&] { delete s; });
+}
+
+int vreg_solver_set_images(vreg_solver s, const float* m0, const float* m1) {
+  return guarded([&] {
+    const size_t bytes = s->m0.local_points() * sizeof(float);
+    check(vreg_memcpy_d2d(s->eng.ctx(), s->m0.data(), m0, bytes));
+    check(vreg_memcpy_d2d(s->eng.ctx(), s->m1.data(), m1, bytes));
+  });
+}
+
+int vreg_solver_syn_images(vreg_solver s) {
+  return guarded([&] {
+    CudaEngine& e = s->eng;
+    const vreg_grid g = e.vg();
+    check(vreg_syn_template(e.ctx(), &g, s->m0.data()));
+    DVField v = e.make_vfield();
+    check(vreg_syn_velocity(e.ctx(), &g, v.data()));
+    // syn_reference: solve_state(syn_velocity, syn_template)(., 1) on a
+    // private engine state so the solver's counters stay clean
+    CudaEngine aux = CudaEngine::create(e.grid(), s->dev);
+    Transport tr(aux, v, s->cfg.interp_degree);
+    tr.solve_state(s->m0);
+    const size_t N = s->m0.local_points();
+    check(vreg_memcpy_d2d(e.ctx(), s->m1.data(), tr.state(e.grid().nt), N * sizeof(float)));
+  });
+}
+
+int vreg_solver_images(vreg_solver s, float* m0, float* m1) {
+  return guarded([&] {
+    const size_t bytes = s->m0.local_points() * sizeof(float);
+    if (m0) check(vreg_memcpy_d2d(s->eng.ctx(), m0, s->m0.data(), bytes));
+    if (m1) check(vreg_memcpy_d2d(s->eng.ctx(), m1, s->m1.data(), bytes));
+  });
+}
+
+int vreg_solver_linearize(vreg_solver s, const float* v3, double beta) {
+  return guarded([&] {
+    if (beta <= 0) throw parameter_error("beta must be > 0");
+    CudaEngine& e = s->eng;
+    DVField v = e.make_vfield();
+    check(vreg_memcpy_d2d(e.ctx(), v.data(), v3, 3 * v.local_points() * sizeof(float)));
+    s->beta = beta;
+    s->lin = std::make_unique<Transport>(e, std::move(v), s->cfg.interp_degree);
+    s->J = evaluate_objective(e, *s->lin, s->m0, s->m1, beta, s->cfg);
+    s->grad = evaluate_gradient(e, *s->lin, s->m1, beta, s->cfg);
+    s->lin->gradients();  // state-gradient cache for the matvecs
+    s->prec.reset();
+  });
+}
+
+int vreg_solver_objective(vreg_solver s, double J4[4]) {
+  return guarded([&] {
+    require_lin(s);
+    J4[0] = s->J.total;
+    J4[1] = s->J.mismatch;
+    J4[2] = s->J.regularization;
+    J4[3] = s->J.div_penalty;
+  });
+}
+
+int vreg_solver_gradient(vreg_solver s, float* g3) {
+  return guarded([&] {
+    require_lin(s);
+    check(vreg_memcpy_d2d(s->eng.ctx(), g3, s->grad->data(),
+                          3 * s->grad->local_points() * sizeof(float)));
+  });
+}
+
+int vreg_solver_matvec(vreg_solver s, const float* vt3, float* out3) {
+  return guarded([&] {
+    require_lin(s);
+    CudaEngine& e = s->eng;
+    DVField vt = e.make_vfield();
+    const size_t bytes = 3 * vt.local_points() * sizeof(float);
+    check(vreg_memcpy_d2d(e.ctx(), vt.data(), vt3, bytes));
+    DVField h = hessian_matvec(e, *s->lin, vt, s->beta, s->cfg);
+    check(vreg_memcpy_d2d(e.ctx(), out3, h.data(), bytes));
+  });
+}
+
+int vreg_solver_matvec_host(vreg_solver s, const float* vt3_host, float* out3_host) {
+  return guarded([&] {
+    require_lin(s);
+    CudaEngine& e = s->eng;
+    DVField vt = e.make_vfield();
+    const size_t bytes = 3 * vt.local_points() * sizeof(float);
+    check(vreg_memcpy_h2d(e.ctx(), vt.data(), vt3_host, bytes));
+    DVField h = hessian_matvec(e, *s->lin, vt, s->beta, s->cfg);
+    check(vreg_memcpy_d2h(e.ctx(), out3_host, h.data(), bytes));
+  });
+}
+
+int vreg_solver_precond(vreg_solver s, int kind, const float* r3, double eps_k, float* out3,
+                        uint64_t stats4[4]) {
+  return guarded([&] {
+    require_lin(s);
+    CudaEngine& e = s->eng;
+    if (!s->prec || int(s->prec->kind()) != kind) {
+      s->prec = std::make_unique<Preconditioner>(e, PrecondKind(kind), s->beta, s->cfg.eps_h0,
+                                                 s->cfg.h0_inner_cap);
+      s->prec->refresh(s->lin->state_field(e.grid().nt));
+    }
+    DVField r = e.make_vfield();
+    const size_t bytes = 3 * r.local_points() * sizeof(float);
+    check(vreg_memcpy_d2d(e.ctx(), r.data(), r3, bytes));
+    PrecondStats st;
+    DVField z = s->prec->apply(r, eps_k, st);
+    check(vreg_memcpy_d2d(e.ctx(), out3, z.data(), bytes));
+    if (stats4) {
+      stats4[0] = st.inva_applications;
+      stats4[1] = st.h0_applications;
+      stats4[2] = st.inner_iterations;
+      stats4[3] = st.inner_capped ? 1 : 0;
+    }
+  });
+}
+
+int vreg_solver_register(vreg_solver s, float* v_out3, double rep16[16], uint64_t counters21[21]) {
+  return guarded([&] {
+    CudaEngine& e = s->eng;
+    DVField v;
+    SolverReport r = register_images(e, s->m0, s->m1, s->cfg, &v);
+    if (v_out3)
+      check(vreg_memcpy_d2d(e.ctx(), v_out3, v.data(), 3 * v.local_points() * sizeof(float)));
+    if (rep16) {
+      rep16[0] = r.initial_mismatch;
+      rep16[1] = r.final_mismatch;
+      rep16[2] = r.mism_rel;
+      rep16[3] = r.final_g_rel;
+      rep16[4] = r.total_gn();
+      rep16[5] = r.total_pcg();
+      rep16[6] = r.flagged ? 1 : 0;
+      rep16[7] = r.phases.pc;
+      rep16[8] = r.phases.obj;
+      rep16[9] = r.phases.grad;
+      rep16[10] = r.phases.hess;
+      rep16[11] = r.phases.total;
+      rep16[12] = r.kernels.fft;
+      rep16[13] = r.kernels.fd;
+      rep16[14] = r.kernels.sl;
+      rep16[15] = double(r.levels.size());
+    }
+    if (counters21) dump_counters(r.counters, counters21);
+  });
+}
+
+int vreg_solver_counters(vreg_solver s, uint64_t counters21[21]) {
+  return guarded([&] { dump_counters(s->eng.counters(), counters21); });
+}
+
+int vreg_solver_reset_counters(vreg_solver s) {
+  return guarded([&] { s->eng.counters() = KernelCounters{}; });
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+"""End-to-end parity of the C++ host layer + device kernels (solver C ABI)
+with the unmodified reference: linearisation point, GN matvec, the three
+preconditioners, and fixed-iteration registration solves.
+
+Tolerances (BASELINE.json north_star): per-kernel relative L2 <= 1e-5 in
+fp32; end-to-end mismatch, gradient norm and final velocity within 1e-3 at
+the same GN/PCG counts. Logical kernel counters must equal the reference's
+(they feed the Eq. 8 cost model, proj/src/cost_model.cpp).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import ref
+from paper_2008_12820_b200 import Context
+from paper_2008_12820_b200.solver import Config, Solver
+
+pytestmark = pytest.mark.gpu
+
+BETA = 1e-3
+
+
+def host(t):
+    return t.detach().double().cpu().numpy()
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float32, device="cuda")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+def gnorm(x, n):
+    return float(np.sqrt((np.asarray(x) ** 2).sum() * (2 * np.pi / n) ** 3))
+
+
+@pytest.fixture(scope="module")
+def lin64(ctx):
+    n = 64
+    m0, v, m1 = ref.syn(n)
+    cfg = Config(continuation=False, beta_target=BETA)
+    s = Solver(ctx, n, cfg)
+    s.syn_images()
+    s.linearize(dev(0.5 * v), BETA)
+    r = ref.Session(m0, m1, 0.5 * v, BETA, ref.Config(continuation=False, beta_target=BETA))
+    return n, s, r
+
+
+def test_syn_images_on_device(lin64):
+    n, s, r = lin64
+    m0, _, m1 = ref.syn(n)
+    d0, d1 = s.images()
+    assert rel(host(d0), m0) < 1e-7
+    assert rel(host(d1), m1) < 1e-5
+
+
+def test_objective_gradient(lin64):
+    n, s, r = lin64
+    J, Jr = s.objective(), r.objective()
+    assert abs(J["total"] / Jr["total"] - 1) < 1e-5
+    assert abs(J["mismatch"] / Jr["mismatch"] - 1) < 1e-5
+    assert rel(host(s.gradient()), r.gradient()) < 1e-5
+
+
+def test_matvec_and_goldens(lin64):
+    n, s, r = lin64
+    g = r.gradient()
+    H = host(s.matvec(dev(-g)))
+    assert rel(H, r.matvec(-g)) < 1e-5
+    # SURVEY §8c 64^3 probe goldens
+    assert abs(gnorm(H, n) / 9.8356971587e-2 - 1) < 1e-4
+    assert abs((-g * H).sum() * (2 * np.pi / n) ** 3 / 3.5306942713e-2 - 1) < 1e-4
+
+
+def test_matvec_host_buffers(lin64):
+    n, s, r = lin64
+    g = s.gradient()
+    vt = (-g).contiguous()
+    d = host(s.matvec(vt))
+    h_in = vt.cpu().pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    s.matvec_host(h_in, h_out)
+    assert rel(h_out.double().numpy(), d) < 1e-6
+
+
+@pytest.mark.parametrize("kind", ["inva", "invh0", "2linvh0"])
+def test_preconditioners(lin64, kind):
+    n, s, r = lin64
+    g = r.gradient()
+    out, st = s.precond(kind, dev(-g), 0.5)
+    ref_out, rst = r.precond(kind, -g, 0.5)
+    assert rel(host(out), ref_out) < 1e-4
+    if kind != "inva":
+        assert abs(st["inner"] - rst["inner"]) <= 1
+
+
+@pytest.mark.parametrize("precond,tol", [("2linvh0", 1e-3)])
+def test_fixed_registration_64(ctx, precond, tol):
+    """64^3 SYN, 2 GN x 10 PCG, beta=1e-3, no continuation (BASELINE.json
+    configs[0]; SURVEY §8c golden: mismatch 6.7578035966e-3, g_rel
+    5.87366954e-2, ||v|| 3.7986020295 for 2LInvH0)."""
+    n = 64
+    cfg = Config(continuation=False, beta_target=BETA, fixed_gn=2, fixed_pcg=10, precond=precond)
+    s = Solver(ctx, n, cfg)
+    s.syn_images()
+    v, rep, cnt = s.register()
+    vn = gnorm(host(v), n)
+    golden = {"2linvh0": (6.7578035966e-3, 5.87366954e-2, 3.7986020295)}[precond]
+    assert abs(rep["final_mismatch"] / golden[0] - 1) < tol
+    assert abs(rep["final_g_rel"] / golden[1] - 1) < tol
+    assert abs(vn / golden[2] - 1) < tol
+    assert rep["total_gn"] == 2 and rep["total_pcg"] == 20
+
+
+def test_fixed_registration_counters_match_reference(ctx):
+    """Same logical kernel counts as the reference solve (32^3, InvA and
+    2LInvH0): the cost model of proj/src/cost_model.cpp applies unchanged."""
+    n = 32
+    m0, _, m1 = ref.syn(n)
+    for pc in ("inva", "2linvh0"):
+        cfg = Config(continuation=False, beta_target=BETA, fixed_gn=2, fixed_pcg=3, precond=pc)
+        s = Solver(ctx, n, cfg)
+        s.syn_images()
+        _, rep, cnt = s.register()
+        _, rrep, rcnt = ref.register(m0, m1, ref.Config(continuation=False, beta_target=BETA,
+                                                        fixed_gn=2, fixed_pcg=3, precond=pc))
+        for k in ("fft_forward", "fft_inverse", "fft_forward_coarse", "fft_inverse_coarse",
+                  "fd_gradient", "fd_divergence", "ip_eval", "ip_scatter", "characteristics",
+                  "sl_state", "sl_adjoint", "sl_inc_state", "sl_inc_adjoint", "pc_inva_apply",
+                  "pc_h0_apply", "pc_refresh"):
+            assert cnt[k] == rcnt[k], (pc, k, cnt[k], rcnt[k])
+        assert abs(rep["final_mismatch"] / rrep["final_mismatch"] - 1) < 1e-3
