@@ -208,43 +208,27 @@ def run_reference(args):
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    from paper_2008_12820_b200 import Context
+    from paper_2008_12820_b200.dist import init_from_env
+    from paper_2008_12820_b200.solver import Config, Solver
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-        obj = [Context.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ctx = Context(local, rank, world, obj[0])
-    else:
-        ctx = Context(local)
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE', '1')}")
+    ctx, rank, world, local = init_from_env()
 
     dims = (args.n,) * 3 if world == 1 else weak_grid(args.n, world)
-    g = ctx.grid(*dims, nt=NT)
     deg = args.degree
     Nvox = dims[0] * dims[1] * dims[2]
 
-    # linearisation point, built on device (SYN inputs, syn.cpp:9-49)
-    m0 = ctx.syn_template(g)
-    vsyn = ctx.syn_velocity(g)
-    m1 = ctx.solve_state(g, ctx.characteristics(g, vsyn, deg), m0, deg)[NT].clone()
-    v = (0.5 * vsyn).contiguous()
-    del vsyn
-    fwd = ctx.characteristics(g, v, deg)
-    m = ctx.solve_state(g, fwd, m0, deg)
-    grads = torch.stack([ctx.fd_grad(g, m[t].contiguous()) for t in range(NT + 1)])
-    bwd = ctx.characteristics(g, (-v).contiguous(), deg)
-    q = ctx.adjoint_source_factor(g, v, bwd, deg)
-    lam = ctx.adjoint_sweep(g, bwd, q, (m1 - m[NT]).contiguous(), deg)
-    grad = ctx.integrate_lambda_grad_m(g, lam, grads)
-    ctx.axpy(g, 1.0, ctx.regop(g, v, BETA, False), grad)
-    vt = (-grad).contiguous()
-    del lam, q, bwd, m
+    # linearisation point through the solver C ABI, SYN inputs built on the
+    # device (syn.cpp:9-49): v = 0.5 v_syn, vt = -g
+    solver = Solver(ctx, dims, Config(continuation=False, beta_target=BETA, interp_degree=deg,
+                                      nt=NT))
+    solver.syn_images()
+    g = solver.grid
+    v = (0.5 * ctx.syn_velocity(g)).contiguous()
+    solver.linearize(v, BETA)
+    vt = (-solver.gradient()).contiguous()
+    del v
     out = torch.empty_like(vt)
     stream = torch.cuda.current_stream()
 
@@ -254,7 +238,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def step():
-        ctx.gn_matvec(g, fwd, grads, BETA, vt, deg, out=out)
+        solver.matvec(vt, out)
 
     for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
         step()
@@ -288,12 +272,9 @@ def run_ours(args):
     h_in = torch.empty(vt.shape, dtype=torch.float32, pin_memory=True)
     h_in.copy_(vt)
     h_out = torch.empty(vt.shape, dtype=torch.float32, pin_memory=True)
-    d_in = torch.empty_like(vt)
 
-    def step_e2e():
-        d_in.copy_(h_in, non_blocking=True)
-        ctx.gn_matvec(g, fwd, grads, BETA, d_in, deg, out=out)
-        h_out.copy_(out, non_blocking=True)
+    def step_e2e():  # vreg_solver_matvec_host: H2D, fused matvec, D2H
+        solver.matvec_host(h_in, h_out)
 
     for _ in range(2):
         step_e2e()
@@ -361,6 +342,7 @@ def run_ours(args):
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+    solver.close()
     ctx.close()
     if world > 1:
         dist.destroy_process_group()

@@ -81,10 +81,32 @@ inline vreg_grid to_vg(const Grid3& g) { return vreg_grid{g.n1, g.n2, g.n3, g.nt
 template <int NC>
 class DeviceField {
  public:
-  Grid3 grid;
+  // Host view `.v` of this rank's slab: the reference's templates touch
+  // Field::v directly in one place (Flow::adjoint_source_factor,
+  // transport.hpp:56-60). The first host access downloads the slab; the next
+  // device access uploads it back if it was written. Device kernels never go
+  // through it.
+  class HostMirror {
+   public:
+    size_t size() const { return owner_->n_ * NC; }
+    Real& operator[](size_t i) {
+      owner_->pull();
+      owner_->host_dirty_ = true;
+      return host_[i];
+    }
 
-  DeviceField() = default;
+   private:
+    friend class DeviceField;
+    DeviceField* owner_ = nullptr;
+    std::vector<Real> host_;
+  };
+
+  Grid3 grid;
+  HostMirror v;
+
+  DeviceField() { v.owner_ = this; }
   DeviceField(std::shared_ptr<Device> dev, const Grid3& g) : grid(g), dev_(std::move(dev)) {
+    v.owner_ = this;
     const vreg_grid vg = to_vg(g);
     int n1l = 0, off = 0;
     check(vreg_slab(dev_->ctx(), &vg, &n1l, &off));
@@ -96,6 +118,7 @@ class DeviceField {
     check(vreg_fill(dev_->ctx(), &vg, NC, buf_.get(), 0.0));  // ScalarField(g) zero-fills
   }
   DeviceField(const DeviceField& o) : grid(o.grid), dev_(o.dev_), n_(o.n_) {
+    v.owner_ = this;
     if (!o.buf_) return;
     DeviceField t(o.dev_, o.grid);
     check(vreg_memcpy_d2d(dev_->ctx(), t.data(), o.data(), NC * n_ * sizeof(float)));
@@ -108,13 +131,31 @@ class DeviceField {
     }
     return *this;
   }
-  DeviceField(DeviceField&&) noexcept = default;
-  DeviceField& operator=(DeviceField&&) noexcept = default;
+  DeviceField(DeviceField&& o) noexcept { *this = std::move(o); }
+  DeviceField& operator=(DeviceField&& o) noexcept {
+    grid = o.grid;
+    dev_ = std::move(o.dev_);
+    buf_ = std::move(o.buf_);
+    n_ = o.n_;
+    v.host_ = std::move(o.v.host_);
+    host_valid_ = o.host_valid_;
+    host_dirty_ = o.host_dirty_;
+    v.owner_ = this;
+    o.host_valid_ = o.host_dirty_ = false;
+    return *this;
+  }
 
-  float* data() { return buf_.get(); }
-  const float* data() const { return buf_.get(); }
-  float* comp(int c) { return buf_.get() + size_t(c) * n_; }
-  const float* comp(int c) const { return buf_.get() + size_t(c) * n_; }
+  float* data() {
+    push();
+    host_valid_ = false;  // the device copy may change
+    return buf_.get();
+  }
+  const float* data() const {
+    const_cast<DeviceField*>(this)->push();
+    return buf_.get();
+  }
+  float* comp(int c) { return data() + size_t(c) * n_; }
+  const float* comp(int c) const { return data() + size_t(c) * n_; }
   size_t local_points() const { return n_; }
   index_t size() const { return index_t(n_); }
   bool empty() const { return !buf_; }
@@ -138,9 +179,25 @@ class DeviceField {
   }
 
  private:
+  void pull() {
+    if (host_valid_) return;
+    std::vector<float> tmp(NC * n_);
+    check(vreg_memcpy_d2h(dev_->ctx(), tmp.data(), buf_.get(), NC * n_ * sizeof(float)));
+    v.host_.assign(tmp.begin(), tmp.end());
+    host_valid_ = true;
+  }
+  void push() {
+    if (!host_dirty_) return;
+    std::vector<float> tmp(v.host_.begin(), v.host_.end());
+    check(vreg_memcpy_h2d(dev_->ctx(), buf_.get(), tmp.data(), NC * n_ * sizeof(float)));
+    host_dirty_ = false;
+  }
+
   std::shared_ptr<Device> dev_;
   std::shared_ptr<float> buf_;
   size_t n_ = 0;
+  bool host_valid_ = false;
+  bool host_dirty_ = false;
 };
 
 using DField = DeviceField<1>;

@@ -274,7 +274,7 @@ def regop(v, beta, unit_zero_mode=True):
     shape = v.shape[1:]
     sym = _ksq_half(shape)[3].copy()
     sym[0, 0, 0] = 1.0 if unit_zero_mode else 0.0
-    return np.stack([np.fft.irfftn(np.fft.rfftn(v[c]) * (beta * sym), s=shape)
+    return np.stack([np.fft.irfftn(np.fft.rfftn(v[c]) * (beta * sym), s=shape, axes=(0, 1, 2))
                      for c in range(3)])
 
 
@@ -286,7 +286,7 @@ def inv_regop(w, beta):
     shape = w.shape[1:]
     sym = _ksq_half(shape)[3].copy()
     sym[0, 0, 0] = 1.0
-    return np.stack([np.fft.irfftn(np.fft.rfftn(w[c]) / (beta * sym), s=shape)
+    return np.stack([np.fft.irfftn(np.fft.rfftn(w[c]) / (beta * sym), s=shape, axes=(0, 1, 2))
                      for c in range(3)])
 
 
@@ -316,7 +316,7 @@ def leray(v):
     safe = np.where(ksq == 0, 1.0, ksq)
     kv = (f1 * F[0] + f2 * F[1] + f3 * F[2]) / safe
     kv = np.where(ksq == 0, 0.0, kv)
-    return np.stack([np.fft.irfftn(F[c] - k * kv, s=shape)
+    return np.stack([np.fft.irfftn(F[c] - k * kv, s=shape, axes=(0, 1, 2))
                      for c, k in enumerate((f1, f2, f3))])
 
 

@@ -25,6 +25,7 @@ struct vreg_solver_s {
   std::optional<DVField> grad;
   Real beta = 0;
   std::unique_ptr<Preconditioner> prec;
+  std::optional<DVField> io_in, io_out;  // device staging of the host-buffer matvec
 };
 
 namespace {
@@ -212,9 +213,36 @@ int vreg_solver_gradient(vreg_solver s, float* g3) {
   });
 }
 
+namespace {
+
+// The hot path proper: Transpose adjoint, no div penalty -> the fused device
+// pipeline straight on the caller's buffers (no field copies).
+bool direct_matvec(vreg_solver s, const float* vt3, float* out3) {
+  const RegistrationConfig& c = s->cfg;
+  if (c.hessian_adjoint != HessianAdjoint::Transpose || c.gamma_div > 0) return false;
+  CudaEngine& e = s->eng;
+  const auto& ch = s->lin->forward();
+  const float* gr = s->lin->gradients();
+  auto& k = e.counters();
+  const std::uint64_t nt = std::uint64_t(e.grid().nt);
+  k.sl_inc_state++;
+  k.sl_inc_adjoint++;
+  k.ip_eval += 2 * nt;
+  k.ip_scatter += nt;
+  k.fft_forward += 3;
+  k.fft_inverse += 3;
+  const vreg_grid g = e.vg();
+  check(vreg_gn_matvec(e.ctx(), &g, ch.dep.data(), ch.flags, s->lin->degree(), gr, s->beta, vt3,
+                       out3));
+  return true;
+}
+
+}  // namespace
+
 int vreg_solver_matvec(vreg_solver s, const float* vt3, float* out3) {
   return guarded([&] {
     require_lin(s);
+    if (direct_matvec(s, vt3, out3)) return;
     CudaEngine& e = s->eng;
     DVField vt = e.make_vfield();
     const size_t bytes = 3 * vt.local_points() * sizeof(float);
@@ -228,11 +256,15 @@ int vreg_solver_matvec_host(vreg_solver s, const float* vt3_host, float* out3_ho
   return guarded([&] {
     require_lin(s);
     CudaEngine& e = s->eng;
-    DVField vt = e.make_vfield();
-    const size_t bytes = 3 * vt.local_points() * sizeof(float);
-    check(vreg_memcpy_h2d(e.ctx(), vt.data(), vt3_host, bytes));
-    DVField h = hessian_matvec(e, *s->lin, vt, s->beta, s->cfg);
-    check(vreg_memcpy_d2h(e.ctx(), out3_host, h.data(), bytes));
+    if (!s->io_in) {
+      s->io_in.emplace(e.make_vfield());
+      s->io_out.emplace(e.make_vfield());
+    }
+    const size_t bytes = 3 * s->io_in->local_points() * sizeof(float);
+    check(vreg_memcpy_h2d(e.ctx(), s->io_in->data(), vt3_host, bytes));
+    if (!direct_matvec(s, s->io_in->data(), s->io_out->data()))
+      *s->io_out = hessian_matvec(e, *s->lin, *s->io_in, s->beta, s->cfg);
+    check(vreg_memcpy_d2h(e.ctx(), out3_host, s->io_out->data(), bytes));
   });
 }
 

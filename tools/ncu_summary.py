@@ -1,0 +1,112 @@
+"""Summarise ncu captures into profiles/ (committed evidence).
+
+    python tools/ncu_summary.py <prof.ncu-rep> <launches.csv> <tag>
+
+Writes profiles/<tag>_ncu_full.json (per captured kernel: duration, DRAM
+bytes, throughput %, occupancy, stall mix), profiles/<tag>_launches.json
+(share of device time per kernel over the launch list) and
+profiles/traffic.json (DRAM bytes per launch keyed by bench timer name,
+read by bench.py for roofline.traffic).
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROF = os.path.join(ROOT, "profiles")
+
+METRICS = {
+    "gpu__time_duration.sum": "duration",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_pct",
+    "l1tex__throughput.avg.pct_of_peak_sustained_active": "l1_pct",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
+    "launch__registers_per_thread": "regs",
+    "smsp__inst_executed.sum": "warp_inst",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_bank_conflicts",
+    "sm__issue_active.avg.pct_of_peak_sustained_elapsed": "issue_active_pct",
+}
+STALLS = ["long_scoreboard", "barrier", "mio_throttle", "short_scoreboard", "wait", "selected",
+          "not_selected", "math_pipe_throttle", "lg_throttle"]
+
+# kernel name fragment -> bench.py timer name
+TIMER = {"k_scatter_tile": "sl_scatter_sweep", "k_gather_tile<3, false, 1>": "sl_inc_step",
+         "k_gather_tile<3, 0, 1>": "sl_inc_step", "k_assemble": "sl_assemble"}
+
+
+def unit_scale(u):
+    return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+            "msecond": 1e-3, "second": 1}.get(u, 1)
+
+
+def full(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    out = []
+    for d in rows[2:]:
+        k = {"kernel": d[hdr.index("Kernel Name")][:120]}
+        for m, name in METRICS.items():
+            if m in hdr:
+                i = hdr.index(m)
+                try:
+                    k[name] = float(d[i]) * unit_scale(units[i])
+                except ValueError:
+                    pass
+        for s in STALLS:
+            m = f"smsp__pcsamp_warps_issue_stalled_{s}"
+            if m in hdr:
+                k[f"stall_{s}"] = float(d[hdr.index(m)] or 0)
+        out.append(k)
+    return out
+
+
+def launches(path):
+    text = open(path).read()
+    start = text.find('"ID"')
+    rows = list(csv.reader(io.StringIO(text[start:])))
+    hdr = rows[0]
+    tot = defaultdict(float)
+    cnt = defaultdict(int)
+    for r in rows[1:]:
+        if len(r) < len(hdr) or r[hdr.index("Metric Name")] != "gpu__time_duration.sum":
+            continue
+        name = r[hdr.index("Kernel Name")].split("(")[0][:80]
+        v = float(r[hdr.index("Metric Value")].replace(",", ""))
+        tot[name] += v
+        cnt[name] += 1
+    s = sum(tot.values()) or 1.0
+    return {k: {"launches": cnt[k], "total_ns": tot[k], "share": tot[k] / s}
+            for k in sorted(tot, key=lambda x: -tot[x])}
+
+
+def main():
+    rep, lcsv, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+    os.makedirs(PROF, exist_ok=True)
+    f = full(rep)
+    json.dump(f, open(os.path.join(PROF, f"{tag}_ncu_full.json"), "w"), indent=1)
+    if os.path.exists(lcsv):
+        json.dump(launches(lcsv), open(os.path.join(PROF, f"{tag}_launches.json"), "w"), indent=1)
+    tpath = os.path.join(PROF, "traffic.json")
+    traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
+    for k in f:
+        for frag, timer in TIMER.items():
+            if frag in k["kernel"] and "dram_read" in k:
+                traffic[timer] = k["dram_read"] + k.get("dram_write", 0.0)
+    json.dump(traffic, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
+    for k in f:
+        print(k["kernel"][:60], {x: round(k[x], 1) for x in ("duration", "dram_read", "dram_write",
+                                                           "dram_pct", "warps_active_pct")
+                                 if x in k})
+
+
+if __name__ == "__main__":
+    main()
