@@ -115,6 +115,11 @@ struct vreg_ctx_s {
   cudaStream_t stream = nullptr;
   bool own_stream = true;
   ncclComm_t comm = nullptr;
+  // side stream + dedicated communicator for the regulariser branch of the
+  // matvec (FFTs and their all-to-alls overlap the SL sweeps)
+  cudaStream_t side = nullptr;
+  ncclComm_t fft_comm = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   // FFT plans keyed by (n1, n2, n3, batch); one shared work area
   std::map<std::tuple<int, int, int, int>, vb::FftPlans> plans;

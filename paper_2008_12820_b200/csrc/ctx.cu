@@ -165,6 +165,9 @@ static void init_ctx(vreg_ctx c, int device) {
   VB_CUDA(cudaSetDevice(device));
   VB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;
+  VB_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  VB_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  VB_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   cudaMemPool_t pool;
   VB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
   uint64_t thresh = UINT64_MAX;  // keep freed blocks cached in the pool
@@ -202,6 +205,7 @@ int vreg_ctx_create_dist(int device, int rank, int nranks, const void* uid128,
       ncclUniqueId id;
       std::memcpy(&id, uid128, sizeof(id));
       VB_NCCL(ncclCommInitRank(&c->comm, nranks, id, rank));
+      VB_NCCL(ncclCommSplit(c->comm, 0, rank, &c->fft_comm, nullptr));
     }
     *out = c.release();
   });
@@ -225,8 +229,13 @@ int vreg_ctx_destroy(vreg_ctx ctx) {
       cudaEventDestroy(p.b);
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    cudaStreamSynchronize(ctx->side);
+    if (ctx->fft_comm) ncclCommDestroy(ctx->fft_comm);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    cudaStreamDestroy(ctx->side);
+    cudaEventDestroy(ctx->ev_fork);
+    cudaEventDestroy(ctx->ev_join);
     delete ctx;
   });
 }

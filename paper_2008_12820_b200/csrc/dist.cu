@@ -3,17 +3,16 @@
 //    exact max displacement, "computed, not estimated"), ring
 //    neighbours via grouped ncclSend/ncclRecv;
 //  - reverse halo add for the transpose (scatter) sweeps;
-//  - slab 3-D FFT: batched 2-D R2C on the local x2-x3 planes written directly
-//    in k2-major order, one grouped all-to-all to x2 slabs, batched 1-D C2C
-//    along x1; inverse in reverse order;
+//  - slab 3-D FFT: one batched 2-D R2C over all local x2-x3 planes of all
+//    components, written directly in k2-major order, ONE grouped all-to-all
+//    to x2 slabs, unpack, batched 1-D C2C along x1; inverse in
+//    reverse order;
 //  - all-gather of per-plane fp64 reduction partials (p-independent folds).
 #include <cmath>
 
 #include "common.cuh"
 
 namespace vb {
-
-struct SpecDesc;
 
 namespace {
 
@@ -23,36 +22,42 @@ __global__ void k_add_planes(size_t n, const float* __restrict__ src, float* __r
     dst[i] += src[i];
 }
 
-// [q][k2l][il][h] -> [q*n1l + il][k2l][h]
-__global__ void k_unpack(int p, int n1l, int n2l, int h, const float2* __restrict__ in,
+// received [q][k2l][c*n1l + il][h]  ->  F[c][q*n1l + il][k2l][h]
+__global__ void k_unpack(int p, int ncomp, int n1l, int n2l, int h, const float2* __restrict__ in,
                          float2* __restrict__ out) {
-  const size_t total = size_t(p) * n1l * n2l * h;
+  const size_t nc = size_t(p) * n1l * n2l * h;
+  const size_t total = nc * ncomp;
+  const int B = ncomp * n1l;
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
-    // e indexes the OUTPUT [k1][k2l][k3]
-    const int k3 = int(e % h);
-    const size_t r = e / h;
+    const int c = int(e / nc);
+    size_t r = e - size_t(c) * nc;
+    const int k3 = int(r % h);
+    r /= h;
     const int k2l = int(r % n2l);
     const int k1 = int(r / n2l);
     const int q = k1 / n1l, il = k1 % n1l;
-    out[e] = in[((size_t(q) * n2l + k2l) * n1l + il) * h + k3];
+    out[e] = in[((size_t(q) * n2l + k2l) * B + c * n1l + il) * h + k3];
   }
 }
 
-// [k1][k2l][h] -> [q][k2l][il][h]
-__global__ void k_pack(int p, int n1l, int n2l, int h, const float2* __restrict__ in,
+// F[c][q*n1l + il][k2l][h]  ->  send [q][k2l][c*n1l + il][h]
+__global__ void k_pack(int p, int ncomp, int n1l, int n2l, int h, const float2* __restrict__ in,
                        float2* __restrict__ out) {
-  const size_t total = size_t(p) * n1l * n2l * h;
+  const size_t nc = size_t(p) * n1l * n2l * h;
+  const size_t total = nc * ncomp;
+  const int B = ncomp * n1l;
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
-    // e indexes the OUTPUT [q][k2l][il][k3]
+    // e indexes the OUTPUT [q][k2l][b][k3]
     const int k3 = int(e % h);
     size_t r = e / h;
-    const int il = int(r % n1l);
-    r /= n1l;
+    const int b = int(r % B);
+    r /= B;
     const int k2l = int(r % n2l);
     const int q = int(r / n2l);
-    out[e] = in[((size_t(q) * n1l + il) * n2l + k2l) * h + k3];
+    const int c = b / n1l, il = b % n1l;
+    out[e] = in[size_t(c) * nc + ((size_t(q) * n1l + il) * n2l + k2l) * h + k3];
   }
 }
 
@@ -60,31 +65,29 @@ struct DistPlans {
   cufftHandle r2c2d = 0, c2r2d = 0, c2c1d = 0;
 };
 
-std::map<std::tuple<vreg_ctx, int, int, int>, DistPlans>& dist_plan_map() {
-  static std::map<std::tuple<vreg_ctx, int, int, int>, DistPlans> m;
+std::map<std::tuple<vreg_ctx, int, int, int, int>, DistPlans>& dist_plan_map() {
+  static std::map<std::tuple<vreg_ctx, int, int, int, int>, DistPlans> m;
   return m;
 }
 
-DistPlans& dist_plans(vreg_ctx ctx, const Slab& s) {
-  auto key = std::make_tuple(ctx, s.n1, s.n2, s.n3);
+DistPlans& dist_plans(vreg_ctx ctx, const Slab& s, int ncomp) {
+  auto key = std::make_tuple(ctx, s.n1, s.n2, s.n3, ncomp);
   auto& m = dist_plan_map();
   auto it = m.find(key);
   if (it != m.end()) return it->second;
   const int p = ctx->nranks, n1l = s.n1l, n2l = s.n2 / p, h = s.n3 / 2 + 1;
+  const int B = ncomp * n1l;
   DistPlans d;
   int n2d[2] = {s.n2, s.n3};
   int real_embed[2] = {s.n2, s.n3};
-  int cplx_embed[2] = {s.n2, n1l * h};
+  int cplx_embed[2] = {s.n2, B * h};
   VB_CUFFT(cufftPlanMany(&d.r2c2d, 2, n2d, real_embed, 1, s.n2 * s.n3, cplx_embed, 1, h,
-                         CUFFT_R2C, n1l));
+                         CUFFT_R2C, B));
   VB_CUFFT(cufftPlanMany(&d.c2r2d, 2, n2d, cplx_embed, 1, h, real_embed, 1, s.n2 * s.n3,
-                         CUFFT_C2R, n1l));
+                         CUFFT_C2R, B));
   int n1d[1] = {s.n1};
   int e1[1] = {s.n1};
   VB_CUFFT(cufftPlanMany(&d.c2c1d, 1, n1d, e1, n2l * h, 1, e1, n2l * h, 1, CUFFT_C2C, n2l * h));
-  VB_CUFFT(cufftSetStream(d.r2c2d, ctx->stream));
-  VB_CUFFT(cufftSetStream(d.c2r2d, ctx->stream));
-  VB_CUFFT(cufftSetStream(d.c2c1d, ctx->stream));
   return m.emplace(key, d).first->second;
 }
 
@@ -204,20 +207,21 @@ void dist_fft_forward(vreg_ctx ctx, const Slab& s, int ncomp, const float* f, fl
   require(s.n2 % p == 0, VREG_ECONFIG, "slab FFT needs n2 divisible by the rank count");
   const int n1l = s.n1l, n2l = s.n2 / p, h = s.n3 / 2 + 1;
   const size_t nc = size_t(s.n1) * n2l * h;  // local spectral elements per component
-  DistPlans& d = dist_plans(ctx, s);
-  float2* a = static_cast<float2*>(workspace(ctx, "dfft_a", nc * sizeof(float2)));
-  float2* b = static_cast<float2*>(workspace(ctx, "dfft_b", nc * sizeof(float2)));
+  DistPlans& d = dist_plans(ctx, s, ncomp);
+  float2* a = static_cast<float2*>(workspace(ctx, "dfft_a", ncomp * nc * sizeof(float2)));
+  float2* b = static_cast<float2*>(workspace(ctx, "dfft_b", ncomp * nc * sizeof(float2)));
+  VB_CUFFT(cufftSetStream(d.r2c2d, ctx->stream));
+  VB_CUFFT(cufftExecR2C(d.r2c2d, const_cast<float*>(f), reinterpret_cast<cufftComplex*>(a)));
+  {
+    Timed t(ctx, T_TRANSPOSE);
+    alltoall_chunks(ctx, a, b, size_t(n2l) * ncomp * n1l * h);
+  }
+  k_unpack<<<blocks_for(ncomp * nc, 256), 256, 0, ctx->stream>>>(p, ncomp, n1l, n2l, h, b, F);
+  count_launch(ctx);
+  check_launch();
+  VB_CUFFT(cufftSetStream(d.c2c1d, ctx->stream));
   for (int c = 0; c < ncomp; ++c) {
-    VB_CUFFT(cufftExecR2C(d.r2c2d, const_cast<float*>(f) + size_t(c) * s.local(),
-                          reinterpret_cast<cufftComplex*>(a)));
-    {
-      Timed t(ctx, T_TRANSPOSE);
-      alltoall_chunks(ctx, a, b, size_t(n2l) * n1l * h);
-    }
     float2* Fc = F + size_t(c) * nc;
-    k_unpack<<<blocks_for(nc, 256), 256, 0, ctx->stream>>>(p, n1l, n2l, h, b, Fc);
-    count_launch(ctx);
-    check_launch();
     VB_CUFFT(cufftExecC2C(d.c2c1d, reinterpret_cast<cufftComplex*>(Fc),
                           reinterpret_cast<cufftComplex*>(Fc), CUFFT_FORWARD));
   }
@@ -228,23 +232,24 @@ void dist_fft_inverse(vreg_ctx ctx, const Slab& s, int ncomp, float2* F, float* 
   require(s.n2 % p == 0, VREG_ECONFIG, "slab FFT needs n2 divisible by the rank count");
   const int n1l = s.n1l, n2l = s.n2 / p, h = s.n3 / 2 + 1;
   const size_t nc = size_t(s.n1) * n2l * h;
-  DistPlans& d = dist_plans(ctx, s);
-  float2* a = static_cast<float2*>(workspace(ctx, "dfft_a", nc * sizeof(float2)));
-  float2* b = static_cast<float2*>(workspace(ctx, "dfft_b", nc * sizeof(float2)));
+  DistPlans& d = dist_plans(ctx, s, ncomp);
+  float2* a = static_cast<float2*>(workspace(ctx, "dfft_a", ncomp * nc * sizeof(float2)));
+  float2* b = static_cast<float2*>(workspace(ctx, "dfft_b", ncomp * nc * sizeof(float2)));
+  VB_CUFFT(cufftSetStream(d.c2c1d, ctx->stream));
   for (int c = 0; c < ncomp; ++c) {
     float2* Fc = F + size_t(c) * nc;
     VB_CUFFT(cufftExecC2C(d.c2c1d, reinterpret_cast<cufftComplex*>(Fc),
                           reinterpret_cast<cufftComplex*>(Fc), CUFFT_INVERSE));
-    k_pack<<<blocks_for(nc, 256), 256, 0, ctx->stream>>>(p, n1l, n2l, h, Fc, a);
-    count_launch(ctx);
-    check_launch();
-    {
-      Timed t(ctx, T_TRANSPOSE);
-      alltoall_chunks(ctx, a, b, size_t(n2l) * n1l * h);
-    }
-    VB_CUFFT(cufftExecC2R(d.c2r2d, reinterpret_cast<cufftComplex*>(b),
-                          f + size_t(c) * s.local()));
   }
+  k_pack<<<blocks_for(ncomp * nc, 256), 256, 0, ctx->stream>>>(p, ncomp, n1l, n2l, h, F, a);
+  count_launch(ctx);
+  check_launch();
+  {
+    Timed t(ctx, T_TRANSPOSE);
+    alltoall_chunks(ctx, a, b, size_t(n2l) * ncomp * n1l * h);
+  }
+  VB_CUFFT(cufftSetStream(d.c2r2d, ctx->stream));
+  VB_CUFFT(cufftExecC2R(d.c2r2d, reinterpret_cast<cufftComplex*>(b), f));
 }
 
 }  // namespace vb

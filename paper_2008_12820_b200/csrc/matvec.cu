@@ -21,14 +21,42 @@ void sl_assemble(vreg_ctx ctx, const Slab& s, int descending, const float* sl, c
 void spectral_regop(vreg_ctx ctx, const Slab& s, const float* v3, double beta, bool unit_zero,
                     bool inverse, float* out3);
 
+namespace {
+// Temporarily route the context's stream/communicator to the side branch.
+struct SideRoute {
+  vreg_ctx ctx;
+  cudaStream_t main;
+  ncclComm_t comm;
+  explicit SideRoute(vreg_ctx c) : ctx(c), main(c->stream), comm(c->comm) {
+    c->stream = c->side;
+    if (c->fft_comm) c->comm = c->fft_comm;
+  }
+  ~SideRoute() {
+    ctx->stream = main;
+    ctx->comm = comm;
+  }
+};
+}  // namespace
+
+// The regulariser branch (R2C -> symbol -> C2R, plus the slab all-to-alls
+// on several GPUs) is independent of the transport sweeps until the final
+// assembly, so it runs on a side stream (own NCCL communicator) and
+// overlaps the latency-bound SL kernels.
 void gn_matvec(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int degree,
                const float* grads, double beta, const float* vt3, float* out3) {
   const size_t N = s.local();
   float* psi = static_cast<float*>(workspace(ctx, "mv_psi", size_t(s.nt + 1) * N * sizeof(float)));
   float* reg = static_cast<float*>(workspace(ctx, "mv_reg", 3 * N * sizeof(float)));
-  spectral_regop(ctx, s, vt3, beta, false, false, reg);
+  VB_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
+  VB_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+  {
+    SideRoute route(ctx);
+    spectral_regop(ctx, s, vt3, beta, false, false, reg);
+    VB_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
+  }
   sl_inc_state(ctx, s, disp3, flags, degree, grads, vt3, nullptr, psi + size_t(s.nt) * N);
   sl_transpose_sweeps(ctx, s, disp3, flags, degree, psi);
+  VB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
   sl_assemble(ctx, s, 1, psi, grads, reg, out3);
 }
 

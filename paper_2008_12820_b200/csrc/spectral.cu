@@ -274,6 +274,7 @@ void fft_forward(vreg_ctx ctx, const Slab& s, int ncomp, const float* f, float2*
     return;
   }
   FftPlans& p = fft_plans(ctx, s.n1, s.n2, s.n3, ncomp);
+  VB_CUFFT(cufftSetStream(p.r2c, ctx->stream));  // main or side stream (matvec overlap)
   VB_CUFFT(cufftExecR2C(p.r2c, const_cast<float*>(f), reinterpret_cast<cufftComplex*>(F)));
 }
 
@@ -284,6 +285,7 @@ void fft_inverse(vreg_ctx ctx, const Slab& s, int ncomp, float2* F, float* f) {
     return;
   }
   FftPlans& p = fft_plans(ctx, s.n1, s.n2, s.n3, ncomp);
+  VB_CUFFT(cufftSetStream(p.c2r, ctx->stream));
   VB_CUFFT(cufftExecC2R(p.c2r, reinterpret_cast<cufftComplex*>(F), f));
 }
 

@@ -81,6 +81,26 @@ class Context:
         shape = (n1l, g.n2, g.n3) if ncomp == 1 else (ncomp, n1l, g.n2, g.n3)
         return torch.zeros(shape, dtype=torch.float32, device=f"cuda:{self.device}")
 
+    def to_global(self, g, f):
+        """Global field on the host (numpy float32), slabs gathered over ranks."""
+        import numpy as np
+        ncomp = 3 if f.dim() == 4 else 1
+        shape = (g.n1, g.n2, g.n3) if ncomp == 1 else (3, g.n1, g.n2, g.n3)
+        out = np.zeros(shape, dtype=np.float32)
+        check(lib().vreg_to_global(self.h, C.byref(g), ncomp, _p(f),
+                                   out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def from_global(self, g, a):
+        """This rank's slab of a global host array, as a device field."""
+        import numpy as np
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        ncomp = 3 if a.ndim == 4 else 1
+        out = self.field(g, ncomp)
+        check(lib().vreg_from_global(self.h, C.byref(g), ncomp, a.ctypes.data_as(C.c_void_p),
+                                     _p(out)))
+        return out
+
     def synchronize(self):
         check(lib().vreg_ctx_synchronize(self.h))
 

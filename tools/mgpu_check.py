@@ -1,0 +1,89 @@
+"""Multi-GPU parity check (run under torchrun, one process per GPU):
+the x1-slab decomposed run on p GPUs against a single-GPU run of the same
+problem (rank 0 owns a second, non-distributed context on its GPU).
+
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/mgpu_check.py [n]
+
+Checks (p-independence): SYN inputs, state-derived
+objective, gradient, GN matvec, InvA preconditioner, fixed-iteration solve.
+Prints one JSON line on rank 0; exit status 1 on failure.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2008_12820_b200 import Context  # noqa: E402
+from paper_2008_12820_b200.dist import init_from_env  # noqa: E402
+from paper_2008_12820_b200.solver import Config, Solver  # noqa: E402
+
+
+def run(ctx, dims, beta):
+    cfg = Config(continuation=False, beta_target=beta, precond="inva")
+    s = Solver(ctx, dims, cfg)
+    s.syn_images()
+    g = s.grid
+    v = (0.5 * ctx.syn_velocity(g)).contiguous()
+    s.linearize(v, beta)
+    J = s.objective()
+    grad = s.gradient()
+    vt = (-grad).contiguous()
+    H = s.matvec(vt)
+    P, _ = s.precond("inva", vt, 0.5)
+    m0, m1 = s.images()
+    out = {"J": J, "grad": ctx.to_global(g, grad), "H": ctx.to_global(g, H),
+           "P": ctx.to_global(g, P), "m1": ctx.to_global(g, m1)}
+    s.close()
+    cfg2 = Config(continuation=False, beta_target=beta, precond="inva", fixed_gn=2, fixed_pcg=3)
+    s2 = Solver(ctx, dims, cfg2)
+    s2.syn_images()
+    vv, rep, cnt = s2.register()
+    out["solve"] = rep
+    out["v"] = ctx.to_global(g, vv)
+    s2.close()
+    return out
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a.astype(np.float64) - b) / np.linalg.norm(b))
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+    ctx, rank, world, local = init_from_env()
+    dims = (n, n // 2 * 2 if n >= 16 else n, n)
+    beta = 1e-3
+    dist_out = run(ctx, dims, beta)
+    ok = True
+    res = {"world": world, "grid": dims}
+    if rank == 0:
+        single = Context(local)  # independent single-GPU context on the same device
+        ref = run(single, dims, beta)
+        res["J_rel"] = abs(dist_out["J"]["total"] / ref["J"]["total"] - 1)
+        res["mismatch_rel"] = abs(dist_out["J"]["mismatch"] / ref["J"]["mismatch"] - 1)
+        for k in ("m1", "grad", "H", "P", "v"):
+            res[f"{k}_rel"] = rel(dist_out[k], ref[k].astype(np.float64))
+        res["solve_mismatch_rel"] = abs(dist_out["solve"]["final_mismatch"] /
+                                        ref["solve"]["final_mismatch"] - 1)
+        ok = (res["m1_rel"] < 1e-6 and res["J_rel"] < 1e-6 and res["grad_rel"] < 1e-5 and
+              res["H_rel"] < 1e-5 and res["P_rel"] < 1e-5 and res["v_rel"] < 1e-4 and
+              res["solve_mismatch_rel"] < 1e-4)
+        res["ok"] = ok
+        print(json.dumps(res), flush=True)
+        single.close()
+    flag = torch.tensor([1 if ok else 0], device="cuda")
+    dist.broadcast(flag, 0) if world > 1 else None
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    sys.exit(0 if int(flag.item()) else 1)
+
+
+if __name__ == "__main__":
+    main()
