@@ -2,14 +2,14 @@
 """Benchmark of the GN Hessian-matvec hot path (BASELINE.json north_star).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--n 256] [--degree 3]
+                  [--size 256] [--degree 3]
 
 One step = one Gauss-Newton Hessian matvec (optim.hpp:115-137, Transpose
 adjoint, gradient cache on) at the SYN linearisation point v = 0.5 v_syn,
 vt = -g, nt = 4, cubic, beta = 1e-3, fp32 on device.
 N = 1: the 256^3 configuration (BASELINE.json configs[1]). N > 1: weak
 scaling at 256^3 voxels per GPU, slab-decomposed along x1
-(512x256x256 @2, 512x512x256 @4, 512^3 @8); --n 512 gives the 512^3-per-GPU
+(512x256x256 @2, 512x512x256 @4, 512^3 @8); --size 512 gives the 512^3-per-GPU
 family up to 1024^3 on 8 GPUs.
 
 Metric: matvec throughput in Mvox*matvec/s (grid points x matvecs / s),
@@ -189,7 +189,7 @@ def run_reference(args):
         val, dt, kind, sample = cpu_reference_sample(64, args.steps)
         n = 64
     value = n ** 3 * args.steps / dt / 1e6
-    nx, ny, nz = (args.n,) * 3 if args.gpus == 1 else weak_grid(args.n, args.gpus)
+    nx, ny, nz = (args.size,) * 3 if args.gpus == 1 else weak_grid(args.size, args.gpus)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -215,7 +215,7 @@ def run_ours(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE', '1')}")
     ctx, rank, world, local = init_from_env()
 
-    dims = (args.n,) * 3 if world == 1 else weak_grid(args.n, world)
+    dims = (args.size,) * 3 if world == 1 else weak_grid(args.size, world)
     deg = args.degree
     Nvox = dims[0] * dims[1] * dims[2]
 
@@ -367,7 +367,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--size", type=int, default=256, help="per-GPU cube edge (weak scaling family)")
     ap.add_argument("--degree", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
