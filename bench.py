@@ -290,6 +290,39 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_e2e = float(t.item())
     e2e_value = Nvox * args.steps / (ms_e2e * 1e-3) / 1e6
+
+    # ---- the other two BASELINE metrics (single GPU): 2LInvH0 preconditioner
+    # apply throughput at this linearisation (configs[2]) and the full GNK
+    # registration time with the reference defaults (configs[1]).
+    extra = {}
+    if world == 1 and not args.no_registration:
+        r = (-vt).contiguous()
+        pc, _ = solver.precond("2linvh0", r, 0.5)  # refresh + warm
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        napp = 5
+        inner = 0
+        for _ in range(napp):
+            _, st = solver.precond("2linvh0", r, 0.5)
+            inner += st["inner"]
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        pms = ev0.elapsed_time(ev1) / napp
+        extra["precond_2linvh0"] = {"ms_per_apply": pms, "applies_per_s": 1e3 / pms,
+                                    "inner_cg_per_apply": inner / napp, "eps_k": 0.5}
+        reg = Solver(ctx, dims, Config(interp_degree=deg, nt=NT))  # optim.hpp:17-37 defaults
+        reg.syn_images()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, rep, cnt = reg.register()
+        torch.cuda.synchronize()
+        extra["registration"] = {
+            "seconds": time.perf_counter() - t0, "config": "reference defaults: beta 1 -> 5e-4 "
+            "continuation, 2LInvH0 (InvA above beta 0.5), eps_newton 5e-2, nt 4, cubic",
+            "gn_iters": rep["total_gn"], "pcg_iters": rep["total_pcg"], "levels": rep["levels"],
+            "mism_rel": rep["mism_rel"], "final_g_rel": rep["final_g_rel"],
+            "phases_s": {k: rep[f"t_{k}"] for k in ("pc", "obj", "grad", "hess")}}
+        reg.close()
     nbytes = vt.numel() * 4
 
     if rank == 0:
@@ -340,6 +373,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": nbytes, "ms_per_step": ms_e2e / args.steps},
             "gpu_launches": launches,
             "clocks": clk.summary(),
+            **extra,
         }
         emit(line)
     solver.close()
@@ -370,6 +404,8 @@ def main():
     ap.add_argument("--size", type=int, default=256, help="per-GPU cube edge (weak scaling family)")
     ap.add_argument("--degree", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-registration", action="store_true",
+                    help="skip the registration-time and preconditioner extras")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -114,6 +114,25 @@ def test_fixed_registration_64(ctx, precond, tol):
     assert rep["total_gn"] == 2 and rep["total_pcg"] == 20
 
 
+@pytest.mark.parametrize("variant", [
+    dict(hessian_adjoint=1),                      # optimize-then-discretize adjoint (optim.hpp:125-128)
+    dict(interp_degree=1),                        # trilinear (the paper's large runs)
+    dict(gamma_div=0.5, project_divfree=True),    # div penalty + Leray (optim.hpp:81-84, 104-109)
+])
+def test_solver_variants_match_reference(ctx, variant):
+    n = 32
+    m0, v, m1 = ref.syn(n, 4, variant.get("interp_degree", 3))
+    cfg = Config(continuation=False, beta_target=BETA, **variant)
+    s = Solver(ctx, n, cfg)
+    s.set_images(dev(m0), dev(m1))
+    s.linearize(dev(0.5 * v), BETA)
+    r = ref.Session(m0, m1, 0.5 * v, BETA, ref.Config(continuation=False, beta_target=BETA, **variant))
+    assert abs(s.objective()["total"] / r.objective()["total"] - 1) < 1e-5
+    g = r.gradient()
+    assert rel(host(s.gradient()), g) < 1e-5
+    assert rel(host(s.matvec(dev(-g))), r.matvec(-g)) < 1e-5
+
+
 def test_fixed_registration_counters_match_reference(ctx):
     """Same logical kernel counts as the reference solve (32^3, InvA and
     2LInvH0): the cost model of proj/src/cost_model.cpp applies unchanged."""
