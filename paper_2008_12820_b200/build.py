@@ -45,9 +45,10 @@ def _headers():
 
 
 def _flags(nccl_inc):
+    extra = os.environ.get("VREG_NVCC_EXTRA", "").split()  # experiment variants (-D...)
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--extended-lambda",
                    "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-                   "-I", nccl_inc]
+                   "-I", nccl_inc] + extra
 
 
 def _compile(src, nccl_inc, force):

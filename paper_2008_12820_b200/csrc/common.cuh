@@ -135,6 +135,7 @@ struct vreg_ctx_s {
     int n1, n2, n3, n1l, deg;
     int* table;
     uint64_t used;
+    int smem_words;  // largest box in words: the launches' dynamic smem
   };
   std::vector<TileTable> tile_tables;
   uint64_t tile_clock = 0;

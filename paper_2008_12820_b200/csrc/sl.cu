@@ -283,7 +283,7 @@ __device__ __forceinline__ float tile_gather(const Geo& g, const SrcField<DIST>&
 // Gather kernels: issue the box as cp.async, prefetch the 8 points'
 // displacements meanwhile, then serve all taps from smem.
 template <int DEG, bool DIST, int MODE>  // MODE 0: interp(*q), 1: inc-state step
-__global__ void __launch_bounds__(TILE_THREADS, 3) k_gather_tile(
+__global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_gather_tile(
     Geo g, SrcField<DIST> src, const int* __restrict__ boxes, const float* __restrict__ D,
     const float* __restrict__ qf, float* __restrict__ out, const float* __restrict__ vt,
     const float* __restrict__ gr, float half, int last, float* __restrict__ mt_out) {
@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) k_gather_tile(
   const TileBox b = load_tile_box(boxes, tile_index());
   const bool fits = b.ext[0] > 0;
   if (fits) load_box(g, src, b, fbox);
+  // prefetch the points' displacements while the box streams in
   float d1[TILE_PPT], d2[TILE_PPT], d3[TILE_PPT];
 #pragma unroll
   for (int it = 0; it < TILE_PPT; ++it) {
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) k_gather_tile(
 }
 
 template <int DEG, bool DIST>
-__global__ void __launch_bounds__(TILE_THREADS, 3) k_scatter_tile(Geo g, DstField<DIST> dst,
+__global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_scatter_tile(Geo g, DstField<DIST> dst,
                                                                   const int* __restrict__ boxes,
                                                                   const float* __restrict__ D,
                                                                   const float* __restrict__ z) {
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) k_scatter_tile(Geo g, DstFiel
   const bool fits = b.ext[0] > 0;
   if (threadIdx.x == 0) s_zmax = 0u;
   if (fits) {
-    const int words = b.ext[0] * b.ext[1] * BOX_PITCH;
+    const int words = b.ext[0] * BOX_PLANE;
     for (int c = threadIdx.x; c < words; c += TILE_THREADS) ibox[c] = 0;
   }
   float zv[TILE_PPT], d1[TILE_PPT], d2[TILE_PPT], d3[TILE_PPT];
@@ -380,23 +381,36 @@ inline dim3 tile_grid(const Slab& s) {
 // Box table of the characteristics disp3 (cached per pointer/grid/degree;
 // `refresh` recomputes after the characteristics were rewritten). A stale
 // table only costs speed: points outside their box take the global path.
-const int* tile_table(vreg_ctx ctx, const Slab& s, const float* disp3, int degree, bool refresh) {
+struct TileLaunch {
+  const int* boxes;
+  size_t smem;  // dynamic shared memory bytes: the largest box of the table
+};
+
+TileLaunch tile_table(vreg_ctx ctx, const Slab& s, const float* disp3, int degree, bool refresh) {
   const Geo g = geo_of(s);
   const dim3 grid = tile_grid(s);
-  auto build = [&](int* table) {
+  const size_t ntiles = size_t(grid.x) * grid.y * grid.z;
+  // returns the largest box (words); one small D2H per characteristics
+  auto build = [&](int* table) -> int {
+    int* mw = table + 6 * ntiles;
+    VB_CUDA(cudaMemsetAsync(mw, 0, sizeof(int), ctx->stream));
     if (degree == 3)
-      k_tile_boxes<3><<<grid, TILE_THREADS, 0, ctx->stream>>>(g, disp3, table);
+      k_tile_boxes<3><<<grid, TILE_THREADS, 0, ctx->stream>>>(g, disp3, table, mw);
     else
-      k_tile_boxes<1><<<grid, TILE_THREADS, 0, ctx->stream>>>(g, disp3, table);
+      k_tile_boxes<1><<<grid, TILE_THREADS, 0, ctx->stream>>>(g, disp3, table, mw);
     count_launch(ctx);
     check_launch();
+    int words = 0;
+    VB_CUDA(cudaMemcpyAsync(&words, mw, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    VB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return words > 0 ? words : BOX_PITCH;
   };
   for (auto& t : ctx->tile_tables) {
     if (t.disp == disp3 && t.n1 == s.n1 && t.n2 == s.n2 && t.n3 == s.n3 && t.n1l == s.n1l &&
         t.deg == degree) {
-      if (refresh) build(t.table);
+      if (refresh) t.smem_words = build(t.table);
       t.used = ++ctx->tile_clock;
-      return t.table;
+      return {t.table, size_t(t.smem_words) * sizeof(float)};
     }
   }
   if (ctx->tile_tables.size() >= 16) {
@@ -406,12 +420,12 @@ const int* tile_table(vreg_ctx ctx, const Slab& s, const float* disp3, int degre
     VB_CUDA(cudaFreeAsync(lru->table, ctx->stream));
     ctx->tile_tables.erase(lru);
   }
-  const size_t ntiles = size_t(grid.x) * grid.y * grid.z;
   int* table = nullptr;
-  VB_CUDA(cudaMallocAsync(&table, 6 * ntiles * sizeof(int), ctx->stream));
-  build(table);
-  ctx->tile_tables.push_back({disp3, s.n1, s.n2, s.n3, s.n1l, degree, table, ++ctx->tile_clock});
-  return table;
+  VB_CUDA(cudaMallocAsync(&table, (6 * ntiles + 1) * sizeof(int), ctx->stream));
+  const int words = build(table);
+  ctx->tile_tables.push_back(
+      {disp3, s.n1, s.n2, s.n3, s.n1l, degree, table, ++ctx->tile_clock, words});
+  return {table, size_t(words) * sizeof(float)};
 }
 
 constexpr size_t kTileSmem = kTileCap * sizeof(float);
@@ -545,10 +559,11 @@ void interp_sweep(vreg_ctx ctx, const Slab& s, const float* f, const float* disp
   const Geo g = geo_of(s);
   const dim3 grid = sl_grid(s), block(BX, BY);
   if (use_tile()) {
-    const int* boxes = tile_table(ctx, s, disp3, degree, false);
+    const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
+    const int* boxes = tl.boxes;
     SL_DISPATCH(degree, dist,
                 (tile_kernel(k_gather_tile<DEG, DIST, 0>)<<<tile_grid(s), TILE_THREADS,
-                                                             kTileSmem, ctx->stream>>>(
+                                                             tl.smem, ctx->stream>>>(
                     g, src_of<DIST>(f, gh), boxes, disp3, q, out, nullptr, nullptr, 0.f, 0,
                     nullptr)));
   }
@@ -585,9 +600,10 @@ void scatter_sweep(vreg_ctx ctx, const Slab& s, const float* z, const float* dis
     const Geo g = geo_of(s);
     const dim3 grid = sl_grid(s), block(BX, BY);
     if (use_tile()) {
-      const int* boxes = tile_table(ctx, s, disp3, degree, false);
+      const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
+    const int* boxes = tl.boxes;
       SL_DISPATCH(degree, dist,
-                  (tile_kernel(k_scatter_tile<DEG, DIST>)<<<tile_grid(s), TILE_THREADS, kTileSmem,
+                  (tile_kernel(k_scatter_tile<DEG, DIST>)<<<tile_grid(s), TILE_THREADS, tl.smem,
                                                ctx->stream>>>(g, dst_of<DIST>(out, acc), boxes,
                                                               disp3, z)));
     }
@@ -645,10 +661,11 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
     if (dist) gh = halo_exchange(ctx, s, wt, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
     Timed tm(ctx, T_SL, "sl_inc_step");
     if (use_tile() && !ci.identity) {
-      const int* boxes = tile_table(ctx, s, disp3, degree, false);
+      const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
+    const int* boxes = tl.boxes;
       SL_DISPATCH(degree, dist,
                   (tile_kernel(k_gather_tile<DEG, DIST, 1>)<<<tile_grid(s), TILE_THREADS,
-                                                               kTileSmem, ctx->stream>>>(
+                                                               tl.smem, ctx->stream>>>(
                       g, src_of<DIST>(wt, gh), boxes, disp3, nullptr, wn, vt3,
                       grads + size_t(t + 1) * 3 * N, half, last ? 1 : 0, mo)));
     }

@@ -28,11 +28,23 @@
 
 namespace vb {
 
-constexpr int TT1 = 4, TT2 = 16, TT3 = 32;
-constexpr int TILE_THREADS = 256;
+#ifndef VB_TT1
+#define VB_TT1 4
+#define VB_TT2 16
+#define VB_TILE_THREADS 256
+#endif
+constexpr int TT1 = VB_TT1, TT2 = VB_TT2, TT3 = 32;
+constexpr int TILE_THREADS = VB_TILE_THREADS;
 constexpr int TILE_POINTS = TT1 * TT2 * TT3;
 constexpr int TILE_PPT = TILE_POINTS / TILE_THREADS;  // points per thread (8)
 constexpr int BOX_PITCH = 64;                          // smem row pitch (words)
+// Fixed plane pitch: every tap of a point is an immediate offset from one
+// base register (boxes taller than BOX_ROWS rows take the fallback path).
+constexpr int BOX_ROWS = 24;
+constexpr int BOX_PLANE = BOX_ROWS * BOX_PITCH;
+#ifndef TILE_MIN_BLOCKS
+#define TILE_MIN_BLOCKS 3  // CTAs per SM the register budget is sized for
+#endif
 constexpr int BOX_CAP = 16384;                         // smem words per CTA (64 KB)
 
 // Cached per-tile box: lo1, lo2, lo3, e1, e2, e3 (e1 = 0: empty, e1 < 0: no fit)
@@ -74,7 +86,8 @@ __device__ __forceinline__ int tile_index() {
 
 template <int DEG>
 __global__ void __launch_bounds__(TILE_THREADS) k_tile_boxes(Geo g, const float* __restrict__ D,
-                                                             int* __restrict__ table) {
+                                                             int* __restrict__ table,
+                                                             int* __restrict__ max_words) {
   constexpr int NN = DEG + 1, O0 = DEG == 3 ? -1 : 0;
   __shared__ int smn[3], smx[3];
   if (threadIdx.x < 3) {
@@ -115,9 +128,10 @@ __global__ void __launch_bounds__(TILE_THREADS) k_tile_boxes(Geo g, const float*
     }
     // single-period wrap on load/flush needs every box coordinate in [-n, 2n)
     const int n[3] = {g.n1, g.n2, g.n3};
-    bool fits = e[2] <= BOX_PITCH && e[0] * e[1] * BOX_PITCH <= BOX_CAP;
+    bool fits = e[2] <= BOX_PITCH && e[1] <= BOX_ROWS && e[0] * BOX_PLANE <= BOX_CAP;
     for (int a = 0; a < 3; ++a) fits = fits && e[a] <= n[a] && out[a] >= -n[a] && out[a] + e[a] <= 2 * n[a];
     out[3] = fits ? e[0] : -1;
+    if (fits && max_words) atomicMax(max_words, e[0] * BOX_PLANE);
     out[4] = e[1];
     out[5] = e[2];
   }
@@ -153,7 +167,7 @@ __device__ __forceinline__ void load_box(const Geo& g, const SrcField<DIST>& src
     int p1 = b.lo[0] + u1;
     if constexpr (!DIST) p1 = wrap_once(p1, g.n1);
     const float* P = src.plane_ptr(p1, g);
-    float* SP = sbox + u1 * b.ext[1] * BOX_PITCH;
+    float* SP = sbox + u1 * BOX_PLANE;
     for (int u2 = warp; u2 < b.ext[1]; u2 += TILE_THREADS / 32) {
       const float* R = P + size_t(wrap_once(b.lo[1] + u2, g.n2)) * g.n3;
       float* S = SP + u2 * BOX_PITCH;
@@ -173,7 +187,7 @@ __device__ __forceinline__ void flush_box(const Geo& g, const DstField<DIST>& ds
     int p1 = b.lo[0] + u1;
     if constexpr (!DIST) p1 = wrap_once(p1, g.n1);
     float* P = dst.plane_ptr(p1, g);
-    const int* SP = sbox + u1 * b.ext[1] * BOX_PITCH;
+    const int* SP = sbox + u1 * BOX_PLANE;
     for (int u2 = warp; u2 < b.ext[1]; u2 += TILE_THREADS / 32) {
       float* R = P + size_t(wrap_once(b.lo[1] + u2, g.n2)) * g.n3;
       const int* S = SP + u2 * BOX_PITCH;
@@ -212,12 +226,12 @@ struct BoxStencil {
     lagrange_weights<DEG>(s1, w1);
     lagrange_weights<DEG>(s2, w2);
     lagrange_weights<DEG>(s3, w3);
-    base = (r1 * b.ext[1] + r2) * BOX_PITCH + r3;
+    base = r1 * BOX_PLANE + r2 * BOX_PITCH + r3;
     return in;
   }
 
   __device__ __forceinline__ float gather(const TileBox& b, const float* sbox) const {
-    const int e23 = b.ext[1] * BOX_PITCH;
+    constexpr int e23 = BOX_PLANE;
     float acc1 = 0.f;
 #pragma unroll
     for (int a = 0; a < NN; ++a) {
@@ -236,7 +250,7 @@ struct BoxStencil {
   }
 
   __device__ __forceinline__ void scatter(const TileBox& b, int* sbox, float zS) const {
-    const int e23 = b.ext[1] * BOX_PITCH;
+    constexpr int e23 = BOX_PLANE;
 #pragma unroll
     for (int a = 0; a < NN; ++a) {
       const float za = w1[a] * zS;

@@ -262,6 +262,8 @@ SpecDesc spec_desc(vreg_ctx ctx, const Slab& s) {
 
 void dist_fft_forward(vreg_ctx ctx, const Slab& s, int ncomp, const float* f, float2* F);
 void dist_fft_inverse(vreg_ctx ctx, const Slab& s, int ncomp, float2* F, float* f);
+void dist_restrict(vreg_ctx ctx, const Slab& s, int ncomp, const float* f, float* outc);
+void dist_prolong(vreg_ctx ctx, const Slab& s, int ncomp, const float* fc, float* outf);
 
 float2* spec_buffer(vreg_ctx ctx, const SpecDesc& d, int ncomp, const char* name) {
   return static_cast<float2*>(workspace(ctx, name, d.nc * size_t(ncomp) * sizeof(float2)));
@@ -380,8 +382,10 @@ int vreg_leray(vreg_ctx ctx, const vreg_grid* g, const float* v3, float* out3) {
 int vreg_restrict(vreg_ctx ctx, const vreg_grid* g, int ncomp, const float* f, float* outc) {
   return guard([&] {
     Slab s = slab_of(ctx, g);
-    require(ctx->nranks == 1, VREG_ECONFIG, "restrict: multi-rank path not available");
-    require(s.n1 % 4 == 0 || true, VREG_EDIM, "");
+    if (ctx->nranks > 1) {
+      dist_restrict(ctx, s, ncomp, f, outc);
+      return;
+    }
     vreg_grid gc{s.n1 / 2, s.n2 / 2, s.n3 / 2, s.nt};
     Slab sc = slab_of(ctx, &gc);
     const SpecDesc df = spec_desc(ctx, s), dc = spec_desc(ctx, sc);
@@ -400,7 +404,10 @@ int vreg_restrict(vreg_ctx ctx, const vreg_grid* g, int ncomp, const float* f, f
 int vreg_prolong(vreg_ctx ctx, const vreg_grid* g, int ncomp, const float* fc, float* outf) {
   return guard([&] {
     Slab s = slab_of(ctx, g);
-    require(ctx->nranks == 1, VREG_ECONFIG, "prolong: multi-rank path not available");
+    if (ctx->nranks > 1) {
+      dist_prolong(ctx, s, ncomp, fc, outf);
+      return;
+    }
     vreg_grid gc{s.n1 / 2, s.n2 / 2, s.n3 / 2, s.nt};
     Slab sc = slab_of(ctx, &gc);
     const SpecDesc df = spec_desc(ctx, s), dc = spec_desc(ctx, sc);
@@ -419,7 +426,16 @@ int vreg_prolong(vreg_ctx ctx, const vreg_grid* g, int ncomp, const float* fc, f
 int vreg_high_pass(vreg_ctx ctx, const vreg_grid* g, int ncomp, const float* f, float* out) {
   return guard([&] {
     Slab s = slab_of(ctx, g);
-    require(ctx->nranks == 1, VREG_ECONFIG, "high_pass: multi-rank path not available");
+    if (ctx->nranks > 1) {
+      // high_pass(f) = f - prolong(restrict(f)) (test_spectral.cpp:242-247)
+      float* fc = static_cast<float*>(
+          workspace(ctx, "hp_coarse", size_t(ncomp) * s.local() / 8 * sizeof(float)));
+      dist_restrict(ctx, s, ncomp, f, fc);
+      dist_prolong(ctx, s, ncomp, fc, out);
+      int st = vreg_sub(ctx, g, ncomp, f, out, out);
+      require(st == VREG_OK, st, vreg_last_error());
+      return;
+    }
     const SpecDesc d = spec_desc(ctx, s);
     float2* F = spec_buffer(ctx, d, ncomp, "spec_f");
     float2* G = spec_buffer(ctx, d, ncomp, "spec_f2");

@@ -47,7 +47,28 @@ def run(ctx, dims, beta):
     out["solve"] = rep
     out["v"] = ctx.to_global(g, vv)
     s2.close()
+    # two-level preconditioner pieces (distributed restrict/prolong/high pass)
+    rng = np.random.default_rng(5)
+    fg = rng.standard_normal((3,) + tuple(dims)).astype(np.float32)
+    f = ctx.from_global(g, fg)
+    out["restrict"] = ctx.to_global(VregGridC(g), ctx.restrict(g, f))
+    out["high_pass"] = ctx.to_global(g, ctx.high_pass(g, f))
+    cfg3 = Config(continuation=False, beta_target=beta, precond="2linvh0", fixed_gn=2, fixed_pcg=3)
+    s3 = Solver(ctx, dims, cfg3)
+    s3.syn_images()
+    s3.linearize(v, beta)
+    P2, st = s3.precond("2linvh0", vt, 0.5)
+    out["P2"] = ctx.to_global(g, P2)
+    vv3, rep3, _ = s3.register()
+    out["solve2l"] = rep3
+    out["v2l"] = ctx.to_global(g, vv3)
+    s3.close()
     return out
+
+
+def VregGridC(g):
+    from paper_2008_12820_b200 import VregGrid
+    return VregGrid(g.n1 // 2, g.n2 // 2, g.n3 // 2, g.nt)
 
 
 def rel(a, b):
@@ -67,13 +88,17 @@ def main():
         ref = run(single, dims, beta)
         res["J_rel"] = abs(dist_out["J"]["total"] / ref["J"]["total"] - 1)
         res["mismatch_rel"] = abs(dist_out["J"]["mismatch"] / ref["J"]["mismatch"] - 1)
-        for k in ("m1", "grad", "H", "P", "v"):
+        for k in ("m1", "grad", "H", "P", "v", "restrict", "high_pass", "P2", "v2l"):
             res[f"{k}_rel"] = rel(dist_out[k], ref[k].astype(np.float64))
         res["solve_mismatch_rel"] = abs(dist_out["solve"]["final_mismatch"] /
                                         ref["solve"]["final_mismatch"] - 1)
+        res["solve2l_mismatch_rel"] = abs(dist_out["solve2l"]["final_mismatch"] /
+                                          ref["solve2l"]["final_mismatch"] - 1)
         ok = (res["m1_rel"] < 1e-6 and res["J_rel"] < 1e-6 and res["grad_rel"] < 1e-5 and
               res["H_rel"] < 1e-5 and res["P_rel"] < 1e-5 and res["v_rel"] < 1e-4 and
-              res["solve_mismatch_rel"] < 1e-4)
+              res["solve_mismatch_rel"] < 1e-4 and res["restrict_rel"] < 1e-5 and
+              res["high_pass_rel"] < 1e-5 and res["P2_rel"] < 1e-4 and res["v2l_rel"] < 1e-4 and
+              res["solve2l_mismatch_rel"] < 1e-4)
         res["ok"] = ok
         print(json.dumps(res), flush=True)
         single.close()
