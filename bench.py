@@ -295,10 +295,17 @@ def run_ours(args):
     # apply throughput at this linearisation (configs[2]) and the full GNK
     # registration time with the reference defaults (configs[1]).
     extra = {}
-    if world == 1 and not args.no_registration:
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    if not args.no_registration:
         r = (-vt).contiguous()
         pc, _ = solver.precond("2linvh0", r, 0.5)  # refresh + warm
-        torch.cuda.synchronize()
+        barrier()
         ev0.record(stream)
         napp = 5
         inner = 0
@@ -306,18 +313,19 @@ def run_ours(args):
             _, st = solver.precond("2linvh0", r, 0.5)
             inner += st["inner"]
         ev1.record(stream)
-        torch.cuda.synchronize()
-        pms = ev0.elapsed_time(ev1) / napp
+        barrier()
+        pms = max_over_ranks(ev0.elapsed_time(ev1) / napp)
         extra["precond_2linvh0"] = {"ms_per_apply": pms, "applies_per_s": 1e3 / pms,
                                     "inner_cg_per_apply": inner / napp, "eps_k": 0.5}
         reg = Solver(ctx, dims, Config(interp_degree=deg, nt=NT))  # optim.hpp:17-37 defaults
         reg.syn_images()
-        torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
         _, rep, cnt = reg.register()
-        torch.cuda.synchronize()
+        barrier()
         extra["registration"] = {
-            "seconds": time.perf_counter() - t0, "config": "reference defaults: beta 1 -> 5e-4 "
+            "seconds": max_over_ranks(time.perf_counter() - t0),
+            "grid": list(dims), "n_gpus": world, "config": "reference defaults: beta 1 -> 5e-4 "
             "continuation, 2LInvH0 (InvA above beta 0.5), eps_newton 5e-2, nt 4, cubic",
             "gn_iters": rep["total_gn"], "pcg_iters": rep["total_pcg"], "levels": rep["levels"],
             "mism_rel": rep["mism_rel"], "final_g_rel": rep["final_g_rel"],
@@ -372,6 +380,7 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                     "d2h_bytes_per_step": nbytes, "ms_per_step": ms_e2e / args.steps},
             "gpu_launches": launches,
+            "sl_tiles": dict(zip(("built", "over_smem_budget"), ctx.tile_stats())),
             "clocks": clk.summary(),
             **extra,
         }

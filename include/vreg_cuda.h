@@ -80,6 +80,9 @@ int vreg_ctx_reset_kernel_stats(vreg_ctx ctx);
 int vreg_ctx_comm(vreg_ctx ctx, uint64_t out9[9]);
 /* Number of kernel launches issued by this library since creation. */
 int vreg_ctx_launches(vreg_ctx ctx, uint64_t* out);
+/* SL tile boxes built so far and how many exceeded the shared-memory budget
+ * (those tiles run the per-point global-memory path). */
+int vreg_ctx_tile_stats(vreg_ctx ctx, uint64_t* tiles, uint64_t* misfit);
 
 /* ---- stream-ordered pooled device memory (value-semantics churn, SURVEY
  * §7 hard part 6) */

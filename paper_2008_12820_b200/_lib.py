@@ -41,6 +41,7 @@ _SIGS = {
     "vreg_ctx_kernel_stats": (I, [VP, I, C.c_char_p, C.POINTER(C.c_uint64), C.POINTER(D)]),
     "vreg_ctx_reset_kernel_stats": (I, [VP]),
     "vreg_ctx_launches": (I, [VP, C.POINTER(C.c_uint64)]),
+    "vreg_ctx_tile_stats": (I, [VP, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "vreg_alloc": (I, [VP, C.c_size_t, C.POINTER(VP)]),
     "vreg_free": (I, [VP, VP]),
     "vreg_memcpy_d2d": (I, [VP, VP, VP, C.c_size_t]),

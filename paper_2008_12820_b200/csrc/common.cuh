@@ -139,6 +139,7 @@ struct vreg_ctx_s {
   };
   std::vector<TileTable> tile_tables;
   uint64_t tile_clock = 0;
+  uint64_t tiles_built = 0, tiles_misfit = 0;  // boxes over the smem budget
 
   // reduction scratch
   double* h_pinned = nullptr;  // host staging

@@ -315,6 +315,12 @@ int vreg_ctx_launches(vreg_ctx ctx, uint64_t* out) {
   return VREG_OK;
 }
 
+int vreg_ctx_tile_stats(vreg_ctx ctx, uint64_t* tiles, uint64_t* misfit) {
+  if (tiles) *tiles = ctx->tiles_built;
+  if (misfit) *misfit = ctx->tiles_misfit;
+  return VREG_OK;
+}
+
 int vreg_alloc(vreg_ctx ctx, size_t bytes, void** out) {
   return guard([&] {
     VB_CUDA(cudaMallocAsync(out, bytes ? bytes : 16, ctx->stream));

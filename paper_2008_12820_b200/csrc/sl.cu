@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_scatter_tile(
   const bool fits = b.ext[0] > 0;
   if (threadIdx.x == 0) s_zmax = 0u;
   if (fits) {
-    const int words = b.ext[0] * BOX_PLANE;
+    const int words = b.ext[0] * b.ext[1] * BOX_PITCH;
     for (int c = threadIdx.x; c < words; c += TILE_THREADS) ibox[c] = 0;
   }
   float zv[TILE_PPT], d1[TILE_PPT], d2[TILE_PPT], d3[TILE_PPT];
@@ -392,18 +392,20 @@ TileLaunch tile_table(vreg_ctx ctx, const Slab& s, const float* disp3, int degre
   const size_t ntiles = size_t(grid.x) * grid.y * grid.z;
   // returns the largest box (words); one small D2H per characteristics
   auto build = [&](int* table) -> int {
-    int* mw = table + 6 * ntiles;
-    VB_CUDA(cudaMemsetAsync(mw, 0, sizeof(int), ctx->stream));
+    int* mw = table + 6 * ntiles;  // [0] largest box words, [1] misfit tiles
+    VB_CUDA(cudaMemsetAsync(mw, 0, 2 * sizeof(int), ctx->stream));
     if (degree == 3)
       k_tile_boxes<3><<<grid, TILE_THREADS, 0, ctx->stream>>>(g, disp3, table, mw);
     else
       k_tile_boxes<1><<<grid, TILE_THREADS, 0, ctx->stream>>>(g, disp3, table, mw);
     count_launch(ctx);
     check_launch();
-    int words = 0;
-    VB_CUDA(cudaMemcpyAsync(&words, mw, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    int h[2] = {0, 0};
+    VB_CUDA(cudaMemcpyAsync(h, mw, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     VB_CUDA(cudaStreamSynchronize(ctx->stream));
-    return words > 0 ? words : BOX_PITCH;
+    ctx->tiles_built += ntiles;
+    ctx->tiles_misfit += uint64_t(h[1]);
+    return h[0] > 0 ? h[0] : BOX_PITCH;
   };
   for (auto& t : ctx->tile_tables) {
     if (t.disp == disp3 && t.n1 == s.n1 && t.n2 == s.n2 && t.n3 == s.n3 && t.n1l == s.n1l &&
@@ -421,7 +423,7 @@ TileLaunch tile_table(vreg_ctx ctx, const Slab& s, const float* disp3, int degre
     ctx->tile_tables.erase(lru);
   }
   int* table = nullptr;
-  VB_CUDA(cudaMallocAsync(&table, (6 * ntiles + 1) * sizeof(int), ctx->stream));
+  VB_CUDA(cudaMallocAsync(&table, (6 * ntiles + 2) * sizeof(int), ctx->stream));
   const int words = build(table);
   ctx->tile_tables.push_back(
       {disp3, s.n1, s.n2, s.n3, s.n1l, degree, table, ++ctx->tile_clock, words});

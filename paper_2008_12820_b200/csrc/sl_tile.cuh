@@ -38,14 +38,10 @@ constexpr int TILE_THREADS = VB_TILE_THREADS;
 constexpr int TILE_POINTS = TT1 * TT2 * TT3;
 constexpr int TILE_PPT = TILE_POINTS / TILE_THREADS;  // points per thread (8)
 constexpr int BOX_PITCH = 64;                          // smem row pitch (words)
-// Fixed plane pitch: every tap of a point is an immediate offset from one
-// base register (boxes taller than BOX_ROWS rows take the fallback path).
-constexpr int BOX_ROWS = 24;
-constexpr int BOX_PLANE = BOX_ROWS * BOX_PITCH;
 #ifndef TILE_MIN_BLOCKS
 #define TILE_MIN_BLOCKS 3  // CTAs per SM the register budget is sized for
 #endif
-constexpr int BOX_CAP = 16384;                         // smem words per CTA (64 KB)
+constexpr int BOX_CAP = 18432;                         // smem words per CTA (72 KB: 3 CTAs/SM)
 
 // Cached per-tile box: lo1, lo2, lo3, e1, e2, e3 (e1 = 0: empty, e1 < 0: no fit)
 struct TileBox {
@@ -128,10 +124,11 @@ __global__ void __launch_bounds__(TILE_THREADS) k_tile_boxes(Geo g, const float*
     }
     // single-period wrap on load/flush needs every box coordinate in [-n, 2n)
     const int n[3] = {g.n1, g.n2, g.n3};
-    bool fits = e[2] <= BOX_PITCH && e[1] <= BOX_ROWS && e[0] * BOX_PLANE <= BOX_CAP;
+    bool fits = e[2] <= BOX_PITCH && e[0] * e[1] * BOX_PITCH <= BOX_CAP;
     for (int a = 0; a < 3; ++a) fits = fits && e[a] <= n[a] && out[a] >= -n[a] && out[a] + e[a] <= 2 * n[a];
     out[3] = fits ? e[0] : -1;
-    if (fits && max_words) atomicMax(max_words, e[0] * BOX_PLANE);
+    if (fits && max_words) atomicMax(max_words, e[0] * e[1] * BOX_PITCH);
+    if (!fits && max_words) atomicAdd(max_words + 1, 1);  // misfit tiles
     out[4] = e[1];
     out[5] = e[2];
   }
@@ -167,7 +164,7 @@ __device__ __forceinline__ void load_box(const Geo& g, const SrcField<DIST>& src
     int p1 = b.lo[0] + u1;
     if constexpr (!DIST) p1 = wrap_once(p1, g.n1);
     const float* P = src.plane_ptr(p1, g);
-    float* SP = sbox + u1 * BOX_PLANE;
+    float* SP = sbox + u1 * b.ext[1] * BOX_PITCH;
     for (int u2 = warp; u2 < b.ext[1]; u2 += TILE_THREADS / 32) {
       const float* R = P + size_t(wrap_once(b.lo[1] + u2, g.n2)) * g.n3;
       float* S = SP + u2 * BOX_PITCH;
@@ -187,7 +184,7 @@ __device__ __forceinline__ void flush_box(const Geo& g, const DstField<DIST>& ds
     int p1 = b.lo[0] + u1;
     if constexpr (!DIST) p1 = wrap_once(p1, g.n1);
     float* P = dst.plane_ptr(p1, g);
-    const int* SP = sbox + u1 * BOX_PLANE;
+    const int* SP = sbox + u1 * b.ext[1] * BOX_PITCH;
     for (int u2 = warp; u2 < b.ext[1]; u2 += TILE_THREADS / 32) {
       float* R = P + size_t(wrap_once(b.lo[1] + u2, g.n2)) * g.n3;
       const int* S = SP + u2 * BOX_PITCH;
@@ -226,12 +223,12 @@ struct BoxStencil {
     lagrange_weights<DEG>(s1, w1);
     lagrange_weights<DEG>(s2, w2);
     lagrange_weights<DEG>(s3, w3);
-    base = r1 * BOX_PLANE + r2 * BOX_PITCH + r3;
+    base = (r1 * b.ext[1] + r2) * BOX_PITCH + r3;
     return in;
   }
 
   __device__ __forceinline__ float gather(const TileBox& b, const float* sbox) const {
-    constexpr int e23 = BOX_PLANE;
+    const int e23 = b.ext[1] * BOX_PITCH;
     float acc1 = 0.f;
 #pragma unroll
     for (int a = 0; a < NN; ++a) {
@@ -250,7 +247,7 @@ struct BoxStencil {
   }
 
   __device__ __forceinline__ void scatter(const TileBox& b, int* sbox, float zS) const {
-    constexpr int e23 = BOX_PLANE;
+    const int e23 = b.ext[1] * BOX_PITCH;
 #pragma unroll
     for (int a = 0; a < NN; ++a) {
       const float za = w1[a] * zS;

@@ -134,6 +134,12 @@ class Context:
                  "reduce_bytes", "p2p_messages", "alltoall_collectives"]
         return dict(zip(names, list(out)))
 
+    def tile_stats(self):
+        """(tiles built, tiles over the smem budget -> per-point fallback)."""
+        a, b = C.c_uint64(), C.c_uint64()
+        check(lib().vreg_ctx_tile_stats(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def launches(self) -> int:
         out = C.c_uint64()
         check(lib().vreg_ctx_launches(self.h, C.byref(out)))
