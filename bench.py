@@ -47,9 +47,9 @@ def weak_grid(n, N):
 
 def bytes_per_voxel(nt):
     """Algorithmic HBM bytes per grid point of our fused matvec:
-    inc-state init 28 + nt x 44, nt scatter sweeps x 28, assembly
-    16 (nt+1) + 24, spectral symbol pass 3 x 8.06."""
-    return 28 + 44 * nt + 28 * nt + 16 * (nt + 1) + 24 + 3 * 8.06
+    inc-state pre-pass 12 (nt + 1) + 12 + 4 + 4 nt, nt steps x 24, nt scatter
+    sweeps x 28, assembly 16 (nt+1) + 24, spectral symbol pass 3 x 8.06."""
+    return 12 * (nt + 1) + 16 + 4 * nt + 24 * nt + 28 * nt + 16 * (nt + 1) + 24 + 3 * 8.06
 
 
 class ClockSampler:
@@ -342,8 +342,8 @@ def run_ours(args):
             name, st = dom
             per_launch_s = st["seconds"] / max(st["count"], 1)
             Nloc = Nvox // world
-            bpv = {"sl_scatter_sweep": 28.0, "sl_inc_step": 44.0, "sl_assemble": 16.0 * (NT + 1) + 24.0,
-                   "sl_inc_init": 28.0}.get(name)
+            bpv = {"sl_scatter_sweep": 28.0, "sl_inc_step": 24.0, "sl_assemble": 16.0 * (NT + 1) + 24.0,
+                   "sl_inc_init": 12.0 * (NT + 1) + 16 + 4.0 * NT}.get(name)
             traffic = ncu_traffic()
             roof = {"bound": "hbm", "kernel": name, "peak": peak, "peak_kind": peak_kind,
                     "unit": "GB/s", "bytes_per_voxel": bpv,

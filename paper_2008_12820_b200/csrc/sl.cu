@@ -120,6 +120,31 @@ __global__ void __launch_bounds__(BX* BY) k_inc_step(Geo g, SrcField<DIST> wsrc,
   w_next[p] = last ? -m : m - half * u;
 }
 
+// One streaming pass for the whole incremental-state solve:
+// w0 = -dt/2 (vt . grad m_0) and u_t = vt . grad m_t, t = 1..nt (u holds nt
+// slices), so each fused step then loads one float instead of six.
+__global__ void k_inc_u(size_t n4, int nt, const float4* __restrict__ vt,
+                        const float4* __restrict__ gr, float half, float4* __restrict__ w0,
+                        float4* __restrict__ u) {
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n4; p += stride) {
+    const float4 a = vt[p], b = vt[n4 + p], c = vt[2 * n4 + p];
+    for (int t = 0; t <= nt; ++t) {
+      const float4* g = gr + size_t(t) * 3 * n4;
+      const float4 x = g[p], y = g[n4 + p], z = g[2 * n4 + p];
+      float4 r;
+      r.x = a.x * x.x + b.x * y.x + c.x * z.x;
+      r.y = a.y * x.y + b.y * y.y + c.y * z.y;
+      r.z = a.z * x.z + b.z * y.z + c.z * z.z;
+      r.w = a.w * x.w + b.w * y.w + c.w * z.w;
+      if (t == 0)
+        w0[p] = make_float4(-half * r.x, -half * r.y, -half * r.z, -half * r.w);
+      else
+        u[size_t(t - 1) * n4 + p] = r;
+    }
+  }
+}
+
 // w0 = -dt/2 (vt . grad m_0)
 __global__ void k_inc_init(size_t n, const float* __restrict__ vt, const float* __restrict__ gr,
                            float half, float* __restrict__ w0) {
@@ -291,14 +316,16 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_gather_tile(
   const TileBox b = load_tile_box(boxes, tile_index());
   const bool fits = b.ext[0] > 0;
   if (fits) load_box(g, src, b, fbox);
-  // prefetch the points' displacements while the box streams in
-  float d1[TILE_PPT], d2[TILE_PPT], d3[TILE_PPT];
+  // prefetch the points' displacements (and, MODE 2, the precomputed
+  // u = vt . grad m_{t+1} passed in qf) while the box streams in
+  float d1[TILE_PPT], d2[TILE_PPT], d3[TILE_PPT], uu[TILE_PPT];
 #pragma unroll
   for (int it = 0; it < TILE_PPT; ++it) {
     TILE_PT(it)
     d1[it] = ok ? D[p] : 0.f;
     d2[it] = ok ? D[g.N + p] : 0.f;
     d3[it] = ok ? D[2 * g.N + p] : 0.f;
+    if constexpr (MODE == 2) uu[it] = ok ? qf[p] : 0.f;
   }
   cp_async_wait_all();
   __syncthreads();
@@ -315,7 +342,11 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_gather_tile(
     if constexpr (MODE == 0) {
       out[p] = qf ? G * qf[p] : G;
     } else {
-      const float u = vt[p] * gr[p] + vt[g.N + p] * gr[g.N + p] + vt[2 * g.N + p] * gr[2 * g.N + p];
+      float u;
+      if constexpr (MODE == 2)
+        u = uu[it];
+      else
+        u = vt[p] * gr[p] + vt[g.N + p] * gr[g.N + p] + vt[2 * g.N + p] * gr[2 * g.N + p];
       const float m = G - half * u;
       if (mt_out) mt_out[p] = m;
       out[p] = last ? -m : m - half * u;
@@ -644,9 +675,19 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
   const int nt = s.nt;
   const float half = float(0.5 * s.dt());
   float* w = static_cast<float*>(workspace(ctx, "inc_w", 2 * N * sizeof(float)));
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+  // tile path: all u_t in one streaming pass, steps then read one float each
+  const bool fused_u = use_tile() && !ci.identity && N % 4 == 0 && al16(vt3) && al16(grads);
+  float* u = fused_u ? static_cast<float*>(workspace(ctx, "inc_u", size_t(nt) * N * sizeof(float)))
+                     : nullptr;
   {
     Timed t(ctx, T_SL, "sl_inc_init");
-    k_inc_init<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, vt3, grads, half, w);
+    if (fused_u)
+      k_inc_u<<<blocks_for(N / 4, 256), 256, 0, ctx->stream>>>(
+          N / 4, nt, reinterpret_cast<const float4*>(vt3), reinterpret_cast<const float4*>(grads),
+          half, reinterpret_cast<float4*>(w), reinterpret_cast<float4*>(u));
+    else
+      k_inc_init<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, vt3, grads, half, w);
     count_launch(ctx);
     check_launch();
   }
@@ -662,7 +703,14 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
     Ghosts gh;
     if (dist) gh = halo_exchange(ctx, s, wt, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
     Timed tm(ctx, T_SL, "sl_inc_step");
-    if (use_tile() && !ci.identity) {
+    if (fused_u) {
+      const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
+      SL_DISPATCH(degree, dist,
+                  (tile_kernel(k_gather_tile<DEG, DIST, 2>)<<<tile_grid(s), TILE_THREADS,
+                                                               tl.smem, ctx->stream>>>(
+                      g, src_of<DIST>(wt, gh), tl.boxes, disp3, u + size_t(t) * N, wn, nullptr,
+                      nullptr, half, last ? 1 : 0, mo)));
+    } else if (use_tile() && !ci.identity) {
       const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
     const int* boxes = tl.boxes;
       SL_DISPATCH(degree, dist,
