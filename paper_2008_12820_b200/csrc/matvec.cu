@@ -7,6 +7,7 @@
 //   assembly    : out = sum_{t=nt..0} w_t psi_t grad m_t + beta A vt, one pass
 //
 // 2 nt + 2 of our kernels + 2 batched cuFFT calls per matvec.
+#include <cstdlib>
 #include "common.cuh"
 
 namespace vb {
@@ -47,6 +48,17 @@ void gn_matvec(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int d
   const size_t N = s.local();
   float* psi = static_cast<float*>(workspace(ctx, "mv_psi", size_t(s.nt + 1) * N * sizeof(float)));
   float* reg = static_cast<float*>(workspace(ctx, "mv_reg", 3 * N * sizeof(float)));
+  static const bool serial = [] {  // diagnostics: VREG_SERIAL_MATVEC=1 -> no overlap
+    const char* e = std::getenv("VREG_SERIAL_MATVEC");
+    return e && e[0] == '1';
+  }();
+  if (serial) {
+    spectral_regop(ctx, s, vt3, beta, false, false, reg);
+    sl_inc_state(ctx, s, disp3, flags, degree, grads, vt3, nullptr, psi + size_t(s.nt) * N);
+    sl_transpose_sweeps(ctx, s, disp3, flags, degree, psi);
+    sl_assemble(ctx, s, 1, psi, grads, reg, out3);
+    return;
+  }
   VB_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
   VB_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
   {

@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_gather_tile(
     Geo g, SrcField<DIST> src, const int* __restrict__ boxes, const float* __restrict__ D,
     const float* __restrict__ qf, float* __restrict__ out, const float* __restrict__ vt,
     const float* __restrict__ gr, float half, int last, float* __restrict__ mt_out) {
-  extern __shared__ float fbox[];
+  extern __shared__ __align__(16) float fbox[];
   const TileBox b = load_tile_box(boxes, tile_index());
   const bool fits = b.ext[0] > 0;
   if (fits) load_box(g, src, b, fbox);
@@ -359,14 +359,15 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_scatter_tile(
                                                                   const int* __restrict__ boxes,
                                                                   const float* __restrict__ D,
                                                                   const float* __restrict__ z) {
-  extern __shared__ int ibox[];
+  extern __shared__ __align__(16) int ibox[];
   __shared__ unsigned s_zmax;
   const TileBox b = load_tile_box(boxes, tile_index());
   const bool fits = b.ext[0] > 0;
   if (threadIdx.x == 0) s_zmax = 0u;
   if (fits) {
     const int words = b.ext[0] * b.ext[1] * BOX_PITCH;
-    for (int c = threadIdx.x; c < words; c += TILE_THREADS) ibox[c] = 0;
+    int4* ib4 = reinterpret_cast<int4*>(ibox);  // words % 64 == 0
+    for (int c = threadIdx.x; c < words / 4; c += TILE_THREADS) ib4[c] = make_int4(0, 0, 0, 0);
   }
   float zv[TILE_PPT], d1[TILE_PPT], d2[TILE_PPT], d3[TILE_PPT];
   float zm = 0.f;

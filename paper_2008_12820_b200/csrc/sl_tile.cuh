@@ -122,6 +122,11 @@ __global__ void __launch_bounds__(TILE_THREADS) k_tile_boxes(Geo g, const float*
       out[a] = t[a] + smn[a] + O0;
       e[a] = T[a] - 1 + (smx[a] - smn[a]) + NN;
     }
+    if ((g.n3 & 3) == 0) {  // 16-byte rows: x3 origin and extent 4-aligned
+      const int sh = out[2] & 3;
+      out[2] -= sh;
+      e[2] = (e[2] + sh + 3) & ~3;
+    }
     // single-period wrap on load/flush needs every box coordinate in [-n, 2n)
     const int n[3] = {g.n1, g.n2, g.n3};
     bool fits = e[2] <= BOX_PITCH && e[0] * e[1] * BOX_PITCH <= BOX_CAP;
@@ -154,9 +159,44 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // Issue the box load as cp.async (LDGSTS: no register staging); the caller
 // overlaps its own global loads and then calls cp_async_wait_all() +
 // __syncthreads().
+__device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+// Rows of 16-byte chunks (n3 % 4 == 0: boxes are 4-aligned in x3, see
+// k_tile_boxes): a half-warp per box row, 16 rows per CTA pass; the
+// (u1, u2) walk advances without division.
+#define BOX_ROWS16_BEGIN(b)                                                  \
+  const int lane = threadIdx.x & 31, q = lane & 15;                          \
+  const bool act = 4 * q < (b).ext[2];                                       \
+  int u1 = 0, u2 = (threadIdx.x >> 5) * 2 + (lane >> 4);                     \
+  while (u2 >= (b).ext[1]) {                                                 \
+    u2 -= (b).ext[1];                                                        \
+    ++u1;                                                                    \
+  }                                                                          \
+  for (; u1 < (b).ext[0];) {
+#define BOX_ROWS16_END(b)                                                    \
+  u2 += TILE_THREADS / 16;                                                   \
+  while (u2 >= (b).ext[1]) {                                                 \
+    u2 -= (b).ext[1];                                                        \
+    ++u1;                                                                    \
+  }                                                                          \
+  }
+
 template <bool DIST>
 __device__ __forceinline__ void load_box(const Geo& g, const SrcField<DIST>& src,
                                          const TileBox& b, float* sbox) {
+  if ((g.n3 & 3) == 0) {
+    const int c = wrap_once(b.lo[2] + 4 * (threadIdx.x & 15), g.n3);
+    BOX_ROWS16_BEGIN(b)
+    int p1 = b.lo[0] + u1;
+    if constexpr (!DIST) p1 = wrap_once(p1, g.n1);
+    const float* R = src.plane_ptr(p1, g) + size_t(wrap_once(b.lo[1] + u2, g.n2)) * g.n3;
+    if (act) cp_async16(sbox + (u1 * b.ext[1] + u2) * BOX_PITCH + 4 * q, R + c);
+    BOX_ROWS16_END(b)
+    return;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int c0 = wrap_once(b.lo[2] + lane, g.n3);
   int c1 = wrap_once(b.lo[2] + lane + 32, g.n3);
@@ -177,6 +217,21 @@ __device__ __forceinline__ void load_box(const Geo& g, const SrcField<DIST>& src
 template <bool DIST>
 __device__ __forceinline__ void flush_box(const Geo& g, const DstField<DIST>& dst,
                                           const TileBox& b, const int* sbox, float invS) {
+  if ((g.n3 & 3) == 0) {
+    const int c = wrap_once(b.lo[2] + 4 * (threadIdx.x & 15), g.n3);
+    BOX_ROWS16_BEGIN(b)
+    const int4 v = *reinterpret_cast<const int4*>(sbox + (u1 * b.ext[1] + u2) * BOX_PITCH + 4 * q);
+    if (act && (v.x | v.y | v.z | v.w) != 0) {
+      int p1 = b.lo[0] + u1;
+      if constexpr (!DIST) p1 = wrap_once(p1, g.n1);
+      float* R = dst.plane_ptr(p1, g) + size_t(wrap_once(b.lo[1] + u2, g.n2)) * g.n3 + c;
+      atomicAdd(reinterpret_cast<float4*>(R),
+                make_float4(float(v.x) * invS, float(v.y) * invS, float(v.z) * invS,
+                            float(v.w) * invS));
+    }
+    BOX_ROWS16_END(b)
+    return;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int c0 = wrap_once(b.lo[2] + lane, g.n3);
   int c1 = wrap_once(b.lo[2] + lane + 32, g.n3);
@@ -229,6 +284,33 @@ struct BoxStencil {
 
   __device__ __forceinline__ float gather(const TileBox& b, const float* sbox) const {
     const int e23 = b.ext[1] * BOX_PITCH;
+    if constexpr (DEG == 3) {
+      // packed fp32x2 (FFMA2): tap pairs (c0,c1), (c2,c3) of each row with
+      // the outer-product weights w2[bb] w3[c]; planes folded with w1.
+      const float2 w3a = make_float2(w3[0], w3[1]), w3b = make_float2(w3[2], w3[3]);
+      float2 w23[NN][2];
+#pragma unroll
+      for (int bb = 0; bb < NN; ++bb) {
+        const float2 wb = make_float2(w2[bb], w2[bb]);
+        w23[bb][0] = __fmul2_rn(wb, w3a);
+        w23[bb][1] = __fmul2_rn(wb, w3b);
+      }
+      float2 F = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int a = 0; a < NN; ++a) {
+        const float* P = sbox + base + a * e23;
+        float2 acc = __fmul2_rn(w23[0][0], make_float2(P[0], P[1]));
+        acc = __ffma2_rn(w23[0][1], make_float2(P[2], P[3]), acc);
+#pragma unroll
+        for (int bb = 1; bb < NN; ++bb) {
+          const float* R = P + bb * BOX_PITCH;
+          acc = __ffma2_rn(w23[bb][0], make_float2(R[0], R[1]), acc);
+          acc = __ffma2_rn(w23[bb][1], make_float2(R[2], R[3]), acc);
+        }
+        F = __ffma2_rn(make_float2(w1[a], w1[a]), acc, F);
+      }
+      return F.x + F.y;
+    }
     float acc1 = 0.f;
 #pragma unroll
     for (int a = 0; a < NN; ++a) {
@@ -255,8 +337,18 @@ struct BoxStencil {
       for (int bb = 0; bb < NN; ++bb) {
         int* R = sbox + base + a * e23 + bb * BOX_PITCH;
         const float zab = za * w2[bb];
+        if constexpr (DEG == 3) {
+          const float2 zz = make_float2(zab, zab);
+          const float2 pa = __fmul2_rn(zz, make_float2(w3[0], w3[1]));
+          const float2 pb = __fmul2_rn(zz, make_float2(w3[2], w3[3]));
+          atomicAdd(R, __float2int_rn(pa.x));
+          atomicAdd(R + 1, __float2int_rn(pa.y));
+          atomicAdd(R + 2, __float2int_rn(pb.x));
+          atomicAdd(R + 3, __float2int_rn(pb.y));
+        } else {
 #pragma unroll
-        for (int c = 0; c < NN; ++c) atomicAdd(R + c, __float2int_rn(zab * w3[c]));
+          for (int c = 0; c < NN; ++c) atomicAdd(R + c, __float2int_rn(zab * w3[c]));
+        }
       }
     }
   }
