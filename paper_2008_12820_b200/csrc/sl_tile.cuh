@@ -15,7 +15,9 @@
 //          sm_100a, ~4x slower, tools/smem_atomic_bench.cu) with a per-tile
 //          power-of-two scale S = 2^(27-e), max|z_tile| < 2^e, so each
 //          contribution is exact to 2^-28 max|z| and a cell absorbs > 8
-//          max|z| without overflow. The box is flushed once with fp32 REDs:
+//          max|z| without overflow. Each contribution is rounded by one
+//          DFMA against 1.5 * 2^52 (F2I is quarter-rate XU and was the
+//          binding pipe). The box is flushed once with float4 REDs:
 //          ~3 L2 reductions per point instead of 64 (the L2 RED path is
 //          payload-bound at ~6.4 TB/s, tools/red_bench.cu).
 // Smem rows have a pitch of 64 words, so lanes of a warp (32 consecutive x3
@@ -328,27 +330,25 @@ struct BoxStencil {
     return acc1;
   }
 
+  // Fixed-point contributions round(zS w1 w2 w3). The final product and its
+  // rounding run as one DFMA against 1.5 * 2^52 (the low word of the sum is
+  // the rounded integer, two's complement, for |x| < 2^51): F2I sits on the
+  // quarter-rate XU pipe and bound this kernel, DFMA is half-rate FP64.
   __device__ __forceinline__ void scatter(const TileBox& b, int* sbox, float zS) const {
     const int e23 = b.ext[1] * BOX_PITCH;
+    constexpr double MAGIC = 6755399441055744.0;  // 1.5 * 2^52
+    double w3d[NN];
+#pragma unroll
+    for (int c = 0; c < NN; ++c) w3d[c] = double(w3[c]);
 #pragma unroll
     for (int a = 0; a < NN; ++a) {
       const float za = w1[a] * zS;
 #pragma unroll
       for (int bb = 0; bb < NN; ++bb) {
         int* R = sbox + base + a * e23 + bb * BOX_PITCH;
-        const float zab = za * w2[bb];
-        if constexpr (DEG == 3) {
-          const float2 zz = make_float2(zab, zab);
-          const float2 pa = __fmul2_rn(zz, make_float2(w3[0], w3[1]));
-          const float2 pb = __fmul2_rn(zz, make_float2(w3[2], w3[3]));
-          atomicAdd(R, __float2int_rn(pa.x));
-          atomicAdd(R + 1, __float2int_rn(pa.y));
-          atomicAdd(R + 2, __float2int_rn(pb.x));
-          atomicAdd(R + 3, __float2int_rn(pb.y));
-        } else {
+        const double zab = double(za * w2[bb]);
 #pragma unroll
-          for (int c = 0; c < NN; ++c) atomicAdd(R + c, __float2int_rn(zab * w3[c]));
-        }
+        for (int c = 0; c < NN; ++c) atomicAdd(R + c, __double2loint(fma(zab, w3d[c], MAGIC)));
       }
     }
   }
