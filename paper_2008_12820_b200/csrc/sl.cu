@@ -313,9 +313,16 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_gather_tile(
     const float* __restrict__ qf, float* __restrict__ out, const float* __restrict__ vt,
     const float* __restrict__ gr, float half, int last, float* __restrict__ mt_out) {
   extern __shared__ __align__(16) float fbox[];
+  __shared__ const float* rows[BOX_ROWS_MAX];
   const TileBox b = load_tile_box(boxes, tile_index());
   const bool fits = b.ext[0] > 0;
-  if (fits) load_box(g, src, b, fbox);
+  if (fits) {  // uniform per CTA
+    if (box_vec(g)) {
+      box_rows<DIST>(g, src, b, rows);
+      __syncthreads();
+    }
+    load_box(g, src, b, fbox, rows);
+  }
   // prefetch the points' displacements (and, MODE 2, the precomputed
   // u = vt . grad m_{t+1} passed in qf) while the box streams in
   float d1[TILE_PPT], d2[TILE_PPT], d3[TILE_PPT], uu[TILE_PPT];
@@ -361,10 +368,12 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_scatter_tile(
                                                                   const float* __restrict__ z) {
   extern __shared__ __align__(16) int ibox[];
   __shared__ unsigned s_zmax;
+  __shared__ float* rows[BOX_ROWS_MAX];
   const TileBox b = load_tile_box(boxes, tile_index());
   const bool fits = b.ext[0] > 0;
   if (threadIdx.x == 0) s_zmax = 0u;
   if (fits) {
+    if (box_vec(g)) box_rows<DIST>(g, dst, b, rows);  // read after the barriers below
     const int words = b.ext[0] * b.ext[1] * BOX_PITCH;
     int4* ib4 = reinterpret_cast<int4*>(ibox);  // words % 64 == 0
     for (int c = threadIdx.x; c < words / 4; c += TILE_THREADS) ib4[c] = make_int4(0, 0, 0, 0);
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_scatter_tile(
   }
   if (fits) {
     __syncthreads();
-    flush_box(g, dst, b, ibox, invS);
+    flush_box(g, dst, b, ibox, invS, rows);
   }
 }
 

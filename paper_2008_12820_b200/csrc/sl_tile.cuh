@@ -167,36 +167,38 @@ __device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
 }
 
 // Rows of 16-byte chunks (n3 % 4 == 0: boxes are 4-aligned in x3, see
-// k_tile_boxes): a half-warp per box row, 16 rows per CTA pass; the
-// (u1, u2) walk advances without division.
-#define BOX_ROWS16_BEGIN(b)                                                  \
-  const int lane = threadIdx.x & 31, q = lane & 15;                          \
-  const bool act = 4 * q < (b).ext[2];                                       \
-  int u1 = 0, u2 = (threadIdx.x >> 5) * 2 + (lane >> 4);                     \
-  while (u2 >= (b).ext[1]) {                                                 \
-    u2 -= (b).ext[1];                                                        \
-    ++u1;                                                                    \
-  }                                                                          \
-  for (; u1 < (b).ext[0];) {
-#define BOX_ROWS16_END(b)                                                    \
-  u2 += TILE_THREADS / 16;                                                   \
-  while (u2 >= (b).ext[1]) {                                                 \
-    u2 -= (b).ext[1];                                                        \
-    ++u1;                                                                    \
-  }                                                                          \
-  }
+// k_tile_boxes): a half-warp per box row, 16 rows per CTA pass. The global
+// start of every box row (x1 wrap or ghost plane, x2 wrap) is resolved once
+// per tile into a shared row table, so the copy loops are one table load, an
+// add and the 16-byte transfer per row.
+constexpr int BOX_ROWS_MAX = BOX_CAP / BOX_PITCH;
 
-template <bool DIST>
-__device__ __forceinline__ void load_box(const Geo& g, const SrcField<DIST>& src,
-                                         const TileBox& b, float* sbox) {
-  if ((g.n3 & 3) == 0) {
-    const int c = wrap_once(b.lo[2] + 4 * (threadIdx.x & 15), g.n3);
-    BOX_ROWS16_BEGIN(b)
+__device__ __forceinline__ bool box_vec(const Geo& g) { return (g.n3 & 3) == 0; }
+
+template <bool DIST, class Field, class T>
+__device__ __forceinline__ void box_rows(const Geo& g, const Field& f, const TileBox& b, T** rows) {
+  const int nr = b.ext[0] * b.ext[1];
+  for (int r = threadIdx.x; r < nr; r += TILE_THREADS) {
+    const int u1 = r / b.ext[1], u2 = r - u1 * b.ext[1];
     int p1 = b.lo[0] + u1;
     if constexpr (!DIST) p1 = wrap_once(p1, g.n1);
-    const float* R = src.plane_ptr(p1, g) + size_t(wrap_once(b.lo[1] + u2, g.n2)) * g.n3;
-    if (act) cp_async16(sbox + (u1 * b.ext[1] + u2) * BOX_PITCH + 4 * q, R + c);
-    BOX_ROWS16_END(b)
+    rows[r] = f.plane_ptr(p1, g) + size_t(wrap_once(b.lo[1] + u2, g.n2)) * g.n3;
+  }
+}
+
+// box_vec(g): `rows` must be filled (box_rows + __syncthreads) before the call
+template <bool DIST>
+__device__ __forceinline__ void load_box(const Geo& g, const SrcField<DIST>& src,
+                                         const TileBox& b, float* sbox,
+                                         const float* const* rows) {
+  if (box_vec(g)) {
+    const int q = threadIdx.x & 15;
+    if (4 * q < b.ext[2]) {
+      const int c = wrap_once(b.lo[2] + 4 * q, g.n3);
+      const int nr = b.ext[0] * b.ext[1];
+      for (int r = threadIdx.x >> 4; r < nr; r += TILE_THREADS / 16)
+        cp_async16(sbox + r * BOX_PITCH + 4 * q, rows[r] + c);
+    }
     return;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -218,20 +220,21 @@ __device__ __forceinline__ void load_box(const Geo& g, const SrcField<DIST>& src
 
 template <bool DIST>
 __device__ __forceinline__ void flush_box(const Geo& g, const DstField<DIST>& dst,
-                                          const TileBox& b, const int* sbox, float invS) {
-  if ((g.n3 & 3) == 0) {
-    const int c = wrap_once(b.lo[2] + 4 * (threadIdx.x & 15), g.n3);
-    BOX_ROWS16_BEGIN(b)
-    const int4 v = *reinterpret_cast<const int4*>(sbox + (u1 * b.ext[1] + u2) * BOX_PITCH + 4 * q);
-    if (act && (v.x | v.y | v.z | v.w) != 0) {
-      int p1 = b.lo[0] + u1;
-      if constexpr (!DIST) p1 = wrap_once(p1, g.n1);
-      float* R = dst.plane_ptr(p1, g) + size_t(wrap_once(b.lo[1] + u2, g.n2)) * g.n3 + c;
-      atomicAdd(reinterpret_cast<float4*>(R),
-                make_float4(float(v.x) * invS, float(v.y) * invS, float(v.z) * invS,
-                            float(v.w) * invS));
+                                          const TileBox& b, const int* sbox, float invS,
+                                          float* const* rows) {
+  if (box_vec(g)) {
+    const int q = threadIdx.x & 15;
+    if (4 * q < b.ext[2]) {
+      const int c = wrap_once(b.lo[2] + 4 * q, g.n3);
+      const int nr = b.ext[0] * b.ext[1];
+      for (int r = threadIdx.x >> 4; r < nr; r += TILE_THREADS / 16) {
+        const int4 v = *reinterpret_cast<const int4*>(sbox + r * BOX_PITCH + 4 * q);
+        if ((v.x | v.y | v.z | v.w) != 0)
+          atomicAdd(reinterpret_cast<float4*>(rows[r] + c),
+                    make_float4(float(v.x) * invS, float(v.y) * invS, float(v.z) * invS,
+                                float(v.w) * invS));
+      }
     }
-    BOX_ROWS16_END(b)
     return;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
