@@ -1,0 +1,272 @@
+// Separable H1 regulariser: beta (-Lap) v = beta (D_1 + D_2 + D_3) v with
+// D_a = F_a^-1 diag(k_a^2) F_a the 1-D spectral second derivative along x_a.
+//
+// The reference applies beta |k|^2 through a 3-D r2c -> symbol -> c2r
+// (spectral.cpp:48-70). The 3-D DFT is separable and |k|^2 = k1^2 + k2^2 +
+// k3^2 (every k_a^2 is real and even, Nyquist included), so the same
+// operator is three 1-D passes, each one read of v and one read-modify-write
+// of the output (32 B per voxel and component) instead of the six cuFFT
+// passes plus the symbol pass (~56 B/voxel/comp) of the 3-D route.
+//
+// Pass layout: a CTA owns 32 real pencils of length N along the pass axis
+// (x3 pass: 32 consecutive rows; x2 / x1 passes: 32 consecutive x3 columns,
+// 128-byte coalesced rows). Real pencils are paired into 16 complex pencils
+// (D_a is real, so D_a (x + i y) = D_a x + i D_a y). Each complex pencil is
+// transformed by a four-step FFT N = 16 * R2 held in registers: R2-point
+// DFTs over n2, twiddle W_N^{n1 k2}, one shared-memory transpose, 16-point
+// DFTs over n1; the symbol is applied in registers and the inverse runs the
+// same steps backwards, so the pencil crosses shared memory twice.
+#include <cmath>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace vb {
+
+namespace {
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmul_conj(float2 a, float2 b) {  // a * conj(b)
+  return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+
+// exp(SIGN * 2 pi i m / 32), m in [0, 16): compile-time index after unrolling
+template <int SIGN>
+__device__ __forceinline__ float2 unit32(int m) {
+  constexpr float C[16] = {1.000000000e+00f,  9.807852804e-01f,  9.238795325e-01f,
+                           8.314696123e-01f,  7.071067812e-01f,  5.555702330e-01f,
+                           3.826834324e-01f,  1.950903220e-01f,  0.0f,
+                           -1.950903220e-01f, -3.826834324e-01f, -5.555702330e-01f,
+                           -7.071067812e-01f, -8.314696123e-01f, -9.238795325e-01f,
+                           -9.807852804e-01f};
+  constexpr float S[16] = {0.0f,             1.950903220e-01f, 3.826834324e-01f,
+                           5.555702330e-01f, 7.071067812e-01f, 8.314696123e-01f,
+                           9.238795325e-01f, 9.807852804e-01f, 1.000000000e+00f,
+                           9.807852804e-01f, 9.238795325e-01f, 8.314696123e-01f,
+                           7.071067812e-01f, 5.555702330e-01f, 3.826834324e-01f,
+                           1.950903220e-01f};
+  return make_float2(C[m], SIGN * S[m]);
+}
+
+template <int R>
+__host__ __device__ constexpr int bit_reverse(int i) {
+  int r = 0;
+  for (int b = 1; b < R; b <<= 1) {
+    r = (r << 1) | (i & 1);
+    i >>= 1;
+  }
+  return r;
+}
+
+template <int R, int LEN, int SIGN>
+__device__ __forceinline__ void dit_stages(float2 (&b)[R]) {
+  if constexpr (LEN <= R) {
+#pragma unroll
+    for (int i = 0; i < R; i += LEN) {
+#pragma unroll
+      for (int j = 0; j < LEN / 2; ++j) {
+        float2 t = b[i + j + LEN / 2];
+        if (j != 0) t = cmul(t, unit32<SIGN>(j * (32 / LEN)));
+        const float2 u = b[i + j];
+        b[i + j] = make_float2(u.x + t.x, u.y + t.y);
+        b[i + j + LEN / 2] = make_float2(u.x - t.x, u.y - t.y);
+      }
+    }
+    dit_stages<R, LEN * 2, SIGN>(b);
+  }
+}
+
+// In-register DFT of size R (power of two, <= 32), natural order in and out;
+// SIGN -1 forward, +1 inverse (unnormalised).
+template <int R, int SIGN>
+__device__ __forceinline__ void dft(float2 (&a)[R]) {
+  if constexpr (R > 1) {
+    float2 b[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) b[bit_reverse<R>(i)] = a[i];
+    dit_stages<R, 2, SIGN>(b);
+#pragma unroll
+    for (int i = 0; i < R; ++i) a[i] = b[i];
+  }
+}
+
+constexpr int AX_THREADS = 256;
+
+// out (+)= coef * D_ax v over all 3 components (blockIdx.y). coef = beta / N
+// (1-D inverse normalisation folded in). tw[m] = exp(-2 pi i m / N).
+template <int N, int AX>
+__global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 1) k_axis_d2(int n1l, int n2, int n3,
+                                                         const float* __restrict__ v,
+                                                         float* __restrict__ out,
+                                                         const float2* __restrict__ tw,
+                                                         float coef, int accumulate) {
+  constexpr int R2 = N / 16;
+  constexpr int SK = 17, SP = R2 * SK + 1;  // odd float2 pitches: conflict-free
+  extern __shared__ float2 S[];  // 16 * SP
+  const size_t nloc = size_t(n1l) * n2 * n3;
+  const float* vc = v + size_t(blockIdx.y) * nloc;
+  float* oc = out + size_t(blockIdx.y) * nloc;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  // x3 pass: half-warps run along a row (n1 fastest); x2/x1 passes: along
+  // the 16 column pairs of a 128-byte row (p fastest)
+  const int n1 = AX == 3 ? (l & 15) : 2 * w + (l >> 4);
+  const int p = AX == 3 ? 2 * w + (l >> 4) : (l & 15);
+  size_t base, js, qs;
+  if constexpr (AX == 3) {
+    base = size_t(blockIdx.x) * 32 * n3;
+    js = 1;
+    qs = size_t(n3);
+  } else {
+    const int nb = n3 / 32;
+    const int r = blockIdx.x / nb, xb = blockIdx.x - r * nb;
+    base = (AX == 2 ? size_t(r) * n2 * n3 : size_t(r) * n3) + size_t(xb) * 32;
+    js = AX == 2 ? size_t(n3) : size_t(n2) * n3;
+    qs = 1;
+  }
+  const size_t off = base + size_t(2 * p) * qs + size_t(n1) * js;
+
+  if (accumulate) {  // pull the output rows towards L2 while v streams in
+#pragma unroll
+    for (int m = 0; m < R2; ++m) {
+      const float* q = oc + off + size_t(16 * m) * js;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+      if constexpr (AX == 3) asm volatile("prefetch.global.L2 [%0];" ::"l"(q + qs));
+    }
+  }
+  float2 a[R2];
+#pragma unroll
+  for (int m = 0; m < R2; ++m) {
+    const float* q = vc + off + size_t(16 * m) * js;
+    if constexpr (AX == 3)
+      a[m] = make_float2(__ldg(q), __ldg(q + qs));
+    else
+      a[m] = __ldg(reinterpret_cast<const float2*>(q));
+  }
+  dft<R2, -1>(a);
+  float2* Sp = S + p * SP;
+#pragma unroll
+  for (int k2 = 0; k2 < R2; ++k2) {
+    if (k2 != 0 && n1 != 0) a[k2] = cmul(a[k2], __ldg(tw + n1 * k2));
+    Sp[k2 * SK + n1] = a[k2];
+  }
+  __syncthreads();
+  for (int k2 = n1; k2 < R2; k2 += 16) {  // 16-point DFTs over n1, symbol, inverse
+    float2 b[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) b[j] = Sp[k2 * SK + j];
+    dft<16, -1>(b);
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) {
+      const int f = k2 + R2 * k1;
+      const float fs = float(f <= N / 2 ? f : f - N);
+      const float m = coef * fs * fs;
+      b[k1].x *= m;
+      b[k1].y *= m;
+    }
+    dft<16, 1>(b);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) Sp[k2 * SK + j] = b[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k2 = 0; k2 < R2; ++k2) {
+    a[k2] = Sp[k2 * SK + n1];
+    if (k2 != 0 && n1 != 0) a[k2] = cmul_conj(a[k2], __ldg(tw + n1 * k2));
+  }
+  dft<R2, 1>(a);
+#pragma unroll
+  for (int m = 0; m < R2; ++m) {
+    float* q = oc + off + size_t(16 * m) * js;
+    if constexpr (AX == 3) {
+      if (accumulate) {
+        q[0] += a[m].x;
+        q[qs] += a[m].y;
+      } else {
+        q[0] = a[m].x;
+        q[qs] = a[m].y;
+      }
+    } else {
+      float2* q2 = reinterpret_cast<float2*>(q);
+      if (accumulate) {
+        const float2 o = *q2;
+        *q2 = make_float2(o.x + a[m].x, o.y + a[m].y);
+      } else {
+        *q2 = a[m];
+      }
+    }
+  }
+}
+
+bool axis_size_ok(int n) { return n >= 32 && n <= 512 && (n & (n - 1)) == 0; }
+
+const float2* twiddles(vreg_ctx ctx, int n) {
+  const std::string name = "axis_tw_" + std::to_string(n);
+  if (ctx->ws.count(name)) return static_cast<const float2*>(ctx->ws[name].first);
+  float2* d = static_cast<float2*>(workspace(ctx, name, size_t(n) * sizeof(float2)));
+  std::vector<float2> h(n);
+  const double two_pi = 6.283185307179586476925286766559;
+  for (int m = 0; m < n; ++m)
+    h[m] = make_float2(float(std::cos(two_pi * m / n)), float(-std::sin(two_pi * m / n)));
+  VB_CUDA(cudaMemcpy(d, h.data(), size_t(n) * sizeof(float2), cudaMemcpyHostToDevice));
+  return d;
+}
+
+template <int AX>
+void launch_axis(vreg_ctx ctx, const Slab& s, int n, const float* v3, float* out3, double beta,
+                 int accumulate) {
+  const unsigned tiles = AX == 3 ? unsigned(size_t(s.n1l) * s.n2 / 32)
+                                 : unsigned((AX == 2 ? s.n1l : s.n2) * (s.n3 / 32));
+  const dim3 grid(tiles, 3);
+  const float2* tw = twiddles(ctx, n);
+  const float coef = float(beta / double(n));
+#define VB_AXIS_CASE(NN)                                                                   \
+  case NN: {                                                                               \
+    const size_t smem = size_t(16) * ((NN / 16) * 17 + 1) * sizeof(float2);               \
+    static const bool attr = [&] {                                                         \
+      VB_CUDA(cudaFuncSetAttribute(k_axis_d2<NN, AX>,                                      \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); \
+      return true;                                                                         \
+    }();                                                                                   \
+    (void)attr;                                                                            \
+    k_axis_d2<NN, AX><<<grid, AX_THREADS, smem, ctx->stream>>>(s.n1l, s.n2, s.n3, v3, out3, \
+                                                               tw, coef, accumulate);      \
+    break;                                                                                 \
+  }
+  switch (n) {
+    VB_AXIS_CASE(32)
+    VB_AXIS_CASE(64)
+    VB_AXIS_CASE(128)
+    VB_AXIS_CASE(256)
+    VB_AXIS_CASE(512)
+    default:
+      require(false, VREG_EDIM, "axis transform size");
+  }
+#undef VB_AXIS_CASE
+  count_launch(ctx);
+  check_launch();
+}
+
+}  // namespace
+
+// out3 = beta (-Lap) v3 via three 1-D spectral passes; false if the grid is
+// outside the fast path (distributed x1, non power-of-two or > 512 sizes).
+bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, float* out3) {
+  if (ctx->nranks > 1 || !axis_size_ok(s.n1) || !axis_size_ok(s.n2) || !axis_size_ok(s.n3))
+    return false;
+  static const bool off = [] {
+    const char* e = std::getenv("VREG_REGOP_3D");
+    return e && e[0] == '1';
+  }();
+  if (off) return false;
+  Timed t(ctx, T_FFT, "spec_axis");
+  launch_axis<3>(ctx, s, s.n3, v3, out3, beta, 0);
+  launch_axis<2>(ctx, s, s.n2, v3, out3, beta, 1);
+  launch_axis<1>(ctx, s, s.n1, v3, out3, beta, 1);
+  return true;
+}
+
+}  // namespace vb

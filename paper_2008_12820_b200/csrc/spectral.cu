@@ -300,10 +300,15 @@ void apply_symbol(vreg_ctx ctx, const SpecDesc& d, int ncomp, float2* F, double 
   check_launch();
 }
 
-// out3 = beta A v3 (or its inverse); used by the fused matvec too.
+bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, float* out3);
+
+// out3 = beta A v3 (or its inverse); used by the fused matvec too. The
+// forward operator with a zero null-mode symbol is separable and runs as
+// three 1-D spectral passes (spec_axis.cu) where the grid allows.
 void spectral_regop(vreg_ctx ctx, const Slab& s, const float* v3, double beta, bool unit_zero,
                     bool inverse, float* out3) {
   require(beta > 0.0, VREG_EPARAM, "regularization beta must be > 0");
+  if (!inverse && !unit_zero && regop_separable(ctx, s, v3, beta, out3)) return;
   const SpecDesc d = spec_desc(ctx, s);
   float2* F = spec_buffer(ctx, d, 3, "spec3");
   fft_forward(ctx, s, 3, v3, F);
