@@ -1,6 +1,7 @@
 // Context lifecycle, pooled memory, workspace cache, FFT plan cache, kernel
 // timers and slab distribution (EngineState analogue, engine.hpp:14-19;
 // FftPlanCache, fft.cpp:66-72; from_global/to_global, engine.hpp:63-66).
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <iterator>
@@ -165,7 +166,13 @@ static void init_ctx(vreg_ctx c, int device) {
   VB_CUDA(cudaSetDevice(device));
   VB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;
-  VB_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  {
+    const char* e = std::getenv("VREG_SIDE_PRIO");  // diagnostics: "high" side stream
+    int lo = 0, hi = 0;
+    VB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    VB_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking,
+                                         (e && e[0] == 'h') ? hi : lo));
+  }
   VB_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   VB_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   cudaMemPool_t pool;

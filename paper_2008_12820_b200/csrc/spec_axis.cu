@@ -17,6 +17,7 @@
 // DFTs over n1; the symbol is applied in registers and the inverse runs the
 // same steps backwards, so the pencil crosses shared memory twice.
 #include <cmath>
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -96,10 +97,14 @@ __device__ __forceinline__ void dft(float2 (&a)[R]) {
 
 constexpr int AX_THREADS = 256;
 
-// out (+)= coef * D_ax v over all 3 components (blockIdx.y). coef = beta / N
-// (1-D inverse normalisation folded in). tw[m] = exp(-2 pi i m / N).
+// out (+)= coef * D_ax v over all 3 components. coef = beta / N (1-D
+// inverse normalisation folded in); tw[m] = exp(-2 pi i m / N). CTAs walk
+// the (component, tile) list with a grid stride: one tile each when the grid
+// covers the list, a persistent sweep when the grid is capped (the matvec's
+// side stream, so the sweep shares the SMs with the SL kernels).
 template <int N, int AX>
 __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 1) k_axis_d2(int n1l, int n2, int n3,
+                                                         int tiles,
                                                          const float* __restrict__ v,
                                                          float* __restrict__ out,
                                                          const float2* __restrict__ tw,
@@ -108,8 +113,10 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 1) k_axis_d2(int n1
   constexpr int SK = 17, SP = R2 * SK + 1;  // odd float2 pitches: conflict-free
   extern __shared__ float2 S[];  // 16 * SP
   const size_t nloc = size_t(n1l) * n2 * n3;
-  const float* vc = v + size_t(blockIdx.y) * nloc;
-  float* oc = out + size_t(blockIdx.y) * nloc;
+  for (int t = blockIdx.x; t < 3 * tiles; t += gridDim.x) {
+  const int comp = t / tiles, tile = t - comp * tiles;
+  const float* vc = v + size_t(comp) * nloc;
+  float* oc = out + size_t(comp) * nloc;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   // x3 pass: half-warps run along a row (n1 fastest); x2/x1 passes: along
   // the 16 column pairs of a 128-byte row (p fastest)
@@ -117,12 +124,12 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 1) k_axis_d2(int n1
   const int p = AX == 3 ? 2 * w + (l >> 4) : (l & 15);
   size_t base, js, qs;
   if constexpr (AX == 3) {
-    base = size_t(blockIdx.x) * 32 * n3;
+    base = size_t(tile) * 32 * n3;
     js = 1;
     qs = size_t(n3);
   } else {
     const int nb = n3 / 32;
-    const int r = blockIdx.x / nb, xb = blockIdx.x - r * nb;
+    const int r = tile / nb, xb = tile - r * nb;
     base = (AX == 2 ? size_t(r) * n2 * n3 : size_t(r) * n3) + size_t(xb) * 32;
     js = AX == 2 ? size_t(n3) : size_t(n2) * n3;
     qs = 1;
@@ -199,6 +206,8 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 1) k_axis_d2(int n1
       }
     }
   }
+  __syncthreads();  // S is reused by the next tile
+  }
 }
 
 bool axis_size_ok(int n) { return n >= 32 && n <= 512 && (n & (n - 1)) == 0; }
@@ -217,10 +226,18 @@ const float2* twiddles(vreg_ctx ctx, int n) {
 
 template <int AX>
 void launch_axis(vreg_ctx ctx, const Slab& s, int n, const float* v3, float* out3, double beta,
-                 int accumulate) {
-  const unsigned tiles = AX == 3 ? unsigned(size_t(s.n1l) * s.n2 / 32)
-                                 : unsigned((AX == 2 ? s.n1l : s.n2) * (s.n3 / 32));
-  const dim3 grid(tiles, 3);
+                 int accumulate, int ctas_per_sm) {
+  const int tiles = AX == 3 ? int(size_t(s.n1l) * s.n2 / 32)
+                            : (AX == 2 ? s.n1l : s.n2) * (s.n3 / 32);
+  static const char* names[4] = {"", "spec_axis1", "spec_axis2", "spec_axis3"};
+  Timed timer(ctx, T_FFT, names[AX]);
+  int grid = 3 * tiles;
+  if (ctas_per_sm > 0) {
+    int dev = 0, sms = 0;
+    VB_CUDA(cudaGetDevice(&dev));
+    VB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    grid = std::min(grid, sms * ctas_per_sm);
+  }
   const float2* tw = twiddles(ctx, n);
   const float coef = float(beta / double(n));
 #define VB_AXIS_CASE(NN)                                                                   \
@@ -232,8 +249,8 @@ void launch_axis(vreg_ctx ctx, const Slab& s, int n, const float* v3, float* out
       return true;                                                                         \
     }();                                                                                   \
     (void)attr;                                                                            \
-    k_axis_d2<NN, AX><<<grid, AX_THREADS, smem, ctx->stream>>>(s.n1l, s.n2, s.n3, v3, out3, \
-                                                               tw, coef, accumulate);      \
+    k_axis_d2<NN, AX><<<grid, AX_THREADS, smem, ctx->stream>>>(s.n1l, s.n2, s.n3, tiles, v3, \
+                                                               out3, tw, coef, accumulate); \
     break;                                                                                 \
   }
   switch (n) {
@@ -262,10 +279,14 @@ bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, 
     return e && e[0] == '1';
   }();
   if (off) return false;
-  Timed t(ctx, T_FFT, "spec_axis");
-  launch_axis<3>(ctx, s, s.n3, v3, out3, beta, 0);
-  launch_axis<2>(ctx, s, s.n2, v3, out3, beta, 1);
-  launch_axis<1>(ctx, s, s.n1, v3, out3, beta, 1);
+  // VREG_AXIS_CTAS=k caps the grid at k CTAs per SM (persistent sweep)
+  static const int cap = [] {
+    const char* e = std::getenv("VREG_AXIS_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  launch_axis<3>(ctx, s, s.n3, v3, out3, beta, 0, cap);
+  launch_axis<2>(ctx, s, s.n2, v3, out3, beta, 1, cap);
+  launch_axis<1>(ctx, s, s.n1, v3, out3, beta, 1, cap);
   return true;
 }
 
