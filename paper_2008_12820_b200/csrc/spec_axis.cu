@@ -220,7 +220,10 @@ const float2* twiddles(vreg_ctx ctx, int n) {
   const double two_pi = 6.283185307179586476925286766559;
   for (int m = 0; m < n; ++m)
     h[m] = make_float2(float(std::cos(two_pi * m / n)), float(-std::sin(two_pi * m / n)));
-  VB_CUDA(cudaMemcpy(d, h.data(), size_t(n) * sizeof(float2), cudaMemcpyHostToDevice));
+  // stream-ordered: the pool may hand back memory pending kernels still use
+  VB_CUDA(cudaMemcpyAsync(d, h.data(), size_t(n) * sizeof(float2), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  VB_CUDA(cudaStreamSynchronize(ctx->stream));  // once per size; h dies here
   return d;
 }
 

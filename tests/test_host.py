@@ -66,7 +66,8 @@ def test_bench_helpers():
     assert bench.weak_grid(256, 2) == (512, 256, 256)
     assert bench.weak_grid(256, 8) == (512, 512, 512)
     assert bench.weak_grid(512, 8) == (1024, 1024, 1024)
-    assert abs(bench.bytes_per_voxel(4) - 444.18) < 0.01
+    assert bench.bytes_per_voxel(4) == 552  # 88 + 116 nt
+    assert bench.bytes_per_voxel_ours(4) == 500
 
 
 def test_slab_layout():

@@ -1,6 +1,6 @@
 """Summarise ncu captures into profiles/ (committed evidence).
 
-    python tools/ncu_summary.py <prof.ncu-rep> <launches.csv> <tag>
+    python tools/ncu_summary.py <tag> <launches.csv> <prof.ncu-rep> [...]
 
 Writes profiles/<tag>_ncu_full.json (per captured kernel: duration, DRAM
 bytes, throughput %, occupancy, stall mix), profiles/<tag>_launches.json
@@ -12,6 +12,7 @@ import csv
 import io
 import json
 import os
+import re
 import subprocess
 import sys
 from collections import defaultdict
@@ -37,8 +38,13 @@ STALLS = ["long_scoreboard", "barrier", "mio_throttle", "short_scoreboard", "wai
           "not_selected", "math_pipe_throttle", "lg_throttle"]
 
 # kernel name fragment -> bench.py timer name
-TIMER = {"k_scatter_tile": "sl_scatter_sweep", "k_gather_tile<3, false, 1>": "sl_inc_step",
-         "k_gather_tile<3, 0, 1>": "sl_inc_step", "k_assemble": "sl_assemble"}
+# kernel-name pattern -> bench.py timer name (demangled with or without casts)
+TIMER = [(r"k_scatter_tile<(\(int\))?3", "sl_scatter_sweep"),
+         (r"k_gather_tile<(\(int\))?3, (\(bool\))?(0|false), (\(int\))?2>", "sl_inc_step"),
+         (r"k_inc_u", "sl_inc_init"), (r"k_assemble", "sl_assemble"),
+         (r"k_axis_d2<(\(int\))?\d+, (\(int\))?1>", "spec_axis1"),
+         (r"k_axis_d2<(\(int\))?\d+, (\(int\))?2>", "spec_axis2"),
+         (r"k_axis_d2<(\(int\))?\d+, (\(int\))?3>", "spec_axis3")]
 
 
 def unit_scale(u):
@@ -89,22 +95,23 @@ def launches(path):
 
 
 def main():
-    rep, lcsv, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+    tag, lcsv, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
     os.makedirs(PROF, exist_ok=True)
-    f = full(rep)
+    f = [k for rep in reps for k in full(rep)]
     json.dump(f, open(os.path.join(PROF, f"{tag}_ncu_full.json"), "w"), indent=1)
     if os.path.exists(lcsv):
         json.dump(launches(lcsv), open(os.path.join(PROF, f"{tag}_launches.json"), "w"), indent=1)
     tpath = os.path.join(PROF, "traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     for k in f:
-        for frag, timer in TIMER.items():
-            if frag in k["kernel"] and "dram_read" in k:
+        for pat, timer in TIMER:
+            if re.search(pat, k["kernel"]) and "dram_read" in k:
                 traffic[timer] = k["dram_read"] + k.get("dram_write", 0.0)
     json.dump(traffic, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
     for k in f:
         print(k["kernel"][:60], {x: round(k[x], 1) for x in ("duration", "dram_read", "dram_write",
-                                                           "dram_pct", "warps_active_pct")
+                                                           "dram_pct", "warps_active_pct",
+                                                           "issue_active_pct")
                                  if x in k})
 
 
