@@ -223,6 +223,8 @@ def run_ours(args):
     ctx, rank, world, local = init_from_env()
 
     dims = (args.size,) * 3 if world == 1 else weak_grid(args.size, world)
+    if args.grid:  # explicit global grid (diagnostics), e.g. --grid 512,256,256
+        dims = tuple(int(x) for x in args.grid.split(","))
     deg = args.degree
     Nvox = dims[0] * dims[1] * dims[2]
 
@@ -390,6 +392,8 @@ def run_ours(args):
                                        "ours_moved": bytes_per_voxel_ours(NT)},
             "matvec_frac_of_hbm": matvec_bytes / (ms / args.steps * 1e-3) / 1e9 / peak,
             "fft_ms_per_step": fft_s / args.steps * 1e3,
+            "timer_ms_per_step": {k: round((t_after[k] - t_before[k]) / args.steps * 1e3, 4)
+                                  for k in t_after if t_after[k] != t_before[k]},
             "kernel_share": share,
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -428,6 +432,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=256, help="per-GPU cube edge (weak scaling family)")
     ap.add_argument("--degree", type=int, default=3)
+    ap.add_argument("--grid", default="", help="explicit global grid n1,n2,n3 (overrides --size)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-registration", action="store_true",
                     help="skip the registration-time and preconditioner extras")

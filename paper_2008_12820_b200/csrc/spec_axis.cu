@@ -103,7 +103,7 @@ constexpr int AX_THREADS = 256;
 // covers the list, a persistent sweep when the grid is capped (the matvec's
 // side stream, so the sweep shares the SMs with the SL kernels).
 template <int N, int AX>
-__global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 1) k_axis_d2(int n1l, int n2, int n3,
+__global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 2) k_axis_d2(int n1l, int n2, int n3,
                                                          int tiles,
                                                          const float* __restrict__ v,
                                                          float* __restrict__ out,
@@ -227,9 +227,15 @@ const float2* twiddles(vreg_ctx ctx, int n) {
   return d;
 }
 
+// Geometry of the array a pass runs over: n1l planes of n2 x n3 (on p > 1
+// the x1 pass runs on the x2-slab transpose: all n1 planes of n2/p rows).
+struct AxisGeom {
+  int n1l, n2, n3;
+};
+
 template <int AX>
-void launch_axis(vreg_ctx ctx, const Slab& s, int n, const float* v3, float* out3, double beta,
-                 int accumulate, int ctas_per_sm) {
+void launch_axis(vreg_ctx ctx, const AxisGeom& s, int n, const float* v3, float* out3,
+                 double beta, int accumulate, int ctas_per_sm) {
   const int tiles = AX == 3 ? int(size_t(s.n1l) * s.n2 / 32)
                             : (AX == 2 ? s.n1l : s.n2) * (s.n3 / 32);
   static const char* names[4] = {"", "spec_axis1", "spec_axis2", "spec_axis3"};
@@ -270,13 +276,117 @@ void launch_axis(vreg_ctx ctx, const Slab& s, int n, const float* v3, float* out
   check_launch();
 }
 
+// x1-slab [c][i1l][j][k] -> per-peer blocks [q][c][i1l][j_l][k] (j = q n2l + j_l)
+__global__ void k_axis_pack(int p, int n1l, int n2l, int n3, const float4* __restrict__ in,
+                            float4* __restrict__ out) {
+  const int n34 = n3 / 4;
+  const size_t per = size_t(n1l) * p * n2l * n34;  // float4 per component
+  const size_t total = 3 * per;
+  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += size_t(gridDim.x) * blockDim.x) {
+    const int c = int(e / per);
+    size_t r = e - size_t(c) * per;
+    const int k4 = int(r % n34);
+    r /= n34;
+    const int j = int(r % (size_t(p) * n2l));
+    const int i = int(r / (size_t(p) * n2l));
+    const int q = j / n2l, jl = j - q * n2l;
+    out[((((size_t(q) * 3 + c) * n1l + i) * n2l + jl) * n34) + k4] = in[e];
+  }
+}
+
+// out3[c][i1l][j][k] += blocks[q][c][i1l][j_l][k]
+__global__ void k_axis_unpack_add(int p, int n1l, int n2l, int n3, const float4* __restrict__ in,
+                                  float4* __restrict__ out) {
+  const int n34 = n3 / 4;
+  const size_t per = size_t(n1l) * p * n2l * n34;
+  const size_t total = 3 * per;
+  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += size_t(gridDim.x) * blockDim.x) {
+    const int c = int(e / per);
+    size_t r = e - size_t(c) * per;
+    const int k4 = int(r % n34);
+    r /= n34;
+    const int j = int(r % (size_t(p) * n2l));
+    const int i = int(r / (size_t(p) * n2l));
+    const int q = j / n2l, jl = j - q * n2l;
+    const float4 a = in[((((size_t(q) * 3 + c) * n1l + i) * n2l + jl) * n34) + k4];
+    float4 o = out[e];
+    o.x += a.x;
+    o.y += a.y;
+    o.z += a.z;
+    o.w += a.w;
+    out[e] = o;
+  }
+}
+
+// Grouped send/recv of per-(peer, component) blocks of `blk` floats.
+// send_off / recv_off give each block's offset (in floats) for peer q, comp c.
+template <class SendOff, class RecvOff>
+void axis_exchange(vreg_ctx ctx, const float* send, float* recv, size_t blk, SendOff so,
+                   RecvOff ro) {
+  const int p = ctx->nranks;
+  VB_NCCL(ncclGroupStart());
+  for (int q = 0; q < p; ++q) {
+    if (q == ctx->rank) continue;
+    for (int c = 0; c < 3; ++c) {
+      VB_NCCL(ncclSend(send + so(q, c), blk, ncclFloat, q, ctx->comm, ctx->stream));
+      VB_NCCL(ncclRecv(recv + ro(q, c), blk, ncclFloat, q, ctx->comm, ctx->stream));
+    }
+  }
+  VB_NCCL(ncclGroupEnd());
+  for (int c = 0; c < 3; ++c)
+    VB_CUDA(cudaMemcpyAsync(recv + ro(ctx->rank, c), send + so(ctx->rank, c), blk * sizeof(float),
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->comm_bytes[C_FFT_TRANSPOSE] += uint64_t(p - 1) * 3 * blk * sizeof(float);
+  ctx->comm_bytes[C_ALLTOALL] += 1;
+}
+
+// x1 pass on p > 1: transpose the three components to x2 slabs (one grouped
+// exchange of real data), run the pass over all n1 planes there, transpose
+// back and add. Same per-pencil arithmetic and the same accumulation order
+// (D3, + D2, + D1) as one GPU, so the result is independent of p.
+void dist_axis1(vreg_ctx ctx, const Slab& s, const float* v3, float* out3, double beta,
+                int cap) {
+  const int p = ctx->nranks, n1l = s.n1l, n2l = s.n2 / p, n3 = s.n3;
+  const size_t blk = size_t(n1l) * n2l * n3;  // floats per (peer, component)
+  const size_t all = 3 * size_t(p) * blk;
+  float* a = static_cast<float*>(workspace(ctx, "axis_a", all * sizeof(float)));
+  float* b = static_cast<float*>(workspace(ctx, "axis_b", all * sizeof(float)));
+  const unsigned g4 = unsigned(blocks_for(all / 4, 256));
+  k_axis_pack<<<g4, 256, 0, ctx->stream>>>(p, n1l, n2l, n3, reinterpret_cast<const float4*>(v3),
+                                           reinterpret_cast<float4*>(a));
+  count_launch(ctx);
+  check_launch();
+  const size_t comp_x2 = size_t(s.n1) * n2l * n3;  // one component in the x2-slab layout
+  {
+    Timed t(ctx, T_TRANSPOSE);
+    axis_exchange(
+        ctx, a, b, blk, [&](int q, int c) { return (size_t(q) * 3 + c) * blk; },
+        [&](int q, int c) { return size_t(c) * comp_x2 + size_t(q) * blk; });
+  }
+  launch_axis<1>(ctx, AxisGeom{s.n1, n2l, n3}, s.n1, b, a, beta, 0, cap);
+  {
+    Timed t(ctx, T_TRANSPOSE);
+    axis_exchange(
+        ctx, a, b, blk, [&](int q, int c) { return size_t(c) * comp_x2 + size_t(q) * blk; },
+        [&](int q, int c) { return (size_t(q) * 3 + c) * blk; });
+  }
+  k_axis_unpack_add<<<g4, 256, 0, ctx->stream>>>(p, n1l, n2l, n3,
+                                                 reinterpret_cast<const float4*>(b),
+                                                 reinterpret_cast<float4*>(out3));
+  count_launch(ctx);
+  check_launch();
+}
+
 }  // namespace
 
 // out3 = beta (-Lap) v3 via three 1-D spectral passes; false if the grid is
-// outside the fast path (distributed x1, non power-of-two or > 512 sizes).
+// outside the fast path (non power-of-two or > 512 sizes, x2 not divisible
+// by the rank count).
 bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, float* out3) {
-  if (ctx->nranks > 1 || !axis_size_ok(s.n1) || !axis_size_ok(s.n2) || !axis_size_ok(s.n3))
-    return false;
+  if (!axis_size_ok(s.n1) || !axis_size_ok(s.n2) || !axis_size_ok(s.n3)) return false;
+  if (ctx->nranks > 1 && s.n2 % ctx->nranks != 0) return false;
   static const bool off = [] {
     const char* e = std::getenv("VREG_REGOP_3D");
     return e && e[0] == '1';
@@ -287,9 +397,13 @@ bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, 
     const char* e = std::getenv("VREG_AXIS_CTAS");
     return e ? std::atoi(e) : 0;
   }();
-  launch_axis<3>(ctx, s, s.n3, v3, out3, beta, 0, cap);
-  launch_axis<2>(ctx, s, s.n2, v3, out3, beta, 1, cap);
-  launch_axis<1>(ctx, s, s.n1, v3, out3, beta, 1, cap);
+  const AxisGeom loc{s.n1l, s.n2, s.n3};
+  launch_axis<3>(ctx, loc, s.n3, v3, out3, beta, 0, cap);
+  launch_axis<2>(ctx, loc, s.n2, v3, out3, beta, 1, cap);
+  if (ctx->nranks == 1)
+    launch_axis<1>(ctx, loc, s.n1, v3, out3, beta, 1, cap);
+  else
+    dist_axis1(ctx, s, v3, out3, beta, cap);
   return true;
 }
 

@@ -51,6 +51,7 @@ def run(ctx, dims, beta):
     rng = np.random.default_rng(5)
     fg = rng.standard_normal((3,) + tuple(dims)).astype(np.float32)
     f = ctx.from_global(g, fg)
+    out["regop"] = ctx.to_global(g, ctx.regop(g, f, beta, False))  # separable passes
     out["restrict"] = ctx.to_global(VregGridC(g), ctx.restrict(g, f))
     out["high_pass"] = ctx.to_global(g, ctx.high_pass(g, f))
     cfg3 = Config(continuation=False, beta_target=beta, precond="2linvh0", fixed_gn=2, fixed_pcg=3)
@@ -88,7 +89,7 @@ def main():
         ref = run(single, dims, beta)
         res["J_rel"] = abs(dist_out["J"]["total"] / ref["J"]["total"] - 1)
         res["mismatch_rel"] = abs(dist_out["J"]["mismatch"] / ref["J"]["mismatch"] - 1)
-        for k in ("m1", "grad", "H", "P", "v", "restrict", "high_pass", "P2", "v2l"):
+        for k in ("m1", "grad", "H", "P", "v", "regop", "restrict", "high_pass", "P2", "v2l"):
             res[f"{k}_rel"] = rel(dist_out[k], ref[k].astype(np.float64))
         res["solve_mismatch_rel"] = abs(dist_out["solve"]["final_mismatch"] /
                                         ref["solve"]["final_mismatch"] - 1)
@@ -98,7 +99,7 @@ def main():
               res["H_rel"] < 1e-5 and res["P_rel"] < 1e-5 and res["v_rel"] < 1e-4 and
               res["solve_mismatch_rel"] < 1e-4 and res["restrict_rel"] < 1e-5 and
               res["high_pass_rel"] < 1e-5 and res["P2_rel"] < 1e-4 and res["v2l_rel"] < 1e-4 and
-              res["solve2l_mismatch_rel"] < 1e-4)
+              res["solve2l_mismatch_rel"] < 1e-4 and res["regop_rel"] == 0.0)
         res["ok"] = ok
         print(json.dumps(res), flush=True)
         single.close()
