@@ -120,6 +120,17 @@ struct vreg_ctx_s {
   cudaStream_t side = nullptr;
   ncclComm_t fft_comm = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // halo exchanges of the distributed SL sweeps run here, overlapping the
+  // interior tiles (high priority so NCCL's CTAs are scheduled promptly)
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;
+  // regulariser x2-slab transposes by copy engine into the peers' buffers
+  // (CUDA IPC over NVLink, spec_axis.cu): local send/recv buffers, the peers'
+  // receive buffers, a barrier word
+  float* xbuf[2] = {nullptr, nullptr};
+  std::vector<float*> peer_recv;
+  size_t xbytes = 0;
+  int* xflag = nullptr;
 
   // FFT plans keyed by (n1, n2, n3, batch); one shared work area
   std::map<std::tuple<int, int, int, int>, vb::FftPlans> plans;
@@ -231,6 +242,15 @@ Ghosts halo_exchange(vreg_ctx ctx, const Slab& s, const float* f, int G,
 GhostAcc ghost_accumulators(vreg_ctx ctx, const Slab& s, int G, const char* slot);
 // Reverse halo: ship the ghost accumulators to their owners and add them
 // into the owners' boundary planes of out.
+// Reverse halo add in two halves so the exchange can run on another stream:
+// send the ghost accumulators / receive the neighbours' (top, bot), then add.
+struct RevHalo {
+  float* top = nullptr;
+  float* bot = nullptr;
+  int G = 0;
+};
+RevHalo halo_reverse_send(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, const char* slot);
+void halo_reverse_finish(vreg_ctx ctx, const Slab& s, const RevHalo& r, float* out);
 void halo_reverse_add(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, float* out,
                       const char* slot);
 // Ghost width for a semi-Lagrangian sweep: floor(max|disp1|) + degree-dependent

@@ -173,6 +173,13 @@ static void init_ctx(vreg_ctx c, int device) {
     VB_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking,
                                          (e && e[0] == 'h') ? hi : lo));
   }
+  {
+    int lo = 0, hi = 0;
+    VB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    VB_CUDA(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
+    VB_CUDA(cudaEventCreateWithFlags(&c->ev_c0, cudaEventDisableTiming));
+    VB_CUDA(cudaEventCreateWithFlags(&c->ev_c1, cudaEventDisableTiming));
+  }
   VB_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   VB_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   cudaMemPool_t pool;
@@ -223,6 +230,8 @@ int vreg_ctx_destroy(vreg_ctx ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamSynchronize(ctx->comm_stream);
     for (auto& kv : ctx->plans) {
       cufftDestroy(kv.second.r2c);
       cufftDestroy(kv.second.c2r);
@@ -237,10 +246,18 @@ int vreg_ctx_destroy(vreg_ctx ctx) {
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     cudaStreamSynchronize(ctx->side);
+    for (float* q : ctx->peer_recv)
+      if (q) cudaIpcCloseMemHandle(q);
+    for (int i = 0; i < 2; ++i)
+      if (ctx->xbuf[i]) cudaFree(ctx->xbuf[i]);
+    if (ctx->xflag) cudaFree(ctx->xflag);
     if (ctx->fft_comm) ncclCommDestroy(ctx->fft_comm);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     cudaStreamDestroy(ctx->side);
+    cudaStreamDestroy(ctx->comm_stream);
+    cudaEventDestroy(ctx->ev_c0);
+    cudaEventDestroy(ctx->ev_c1);
     cudaEventDestroy(ctx->ev_fork);
     cudaEventDestroy(ctx->ev_join);
     delete ctx;

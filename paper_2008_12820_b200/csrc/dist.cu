@@ -159,31 +159,40 @@ GhostAcc ghost_accumulators(vreg_ctx ctx, const Slab& s, int G, const char* slot
   return a;
 }
 
-void halo_reverse_add(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, float* out,
-                      const char* slot) {
+RevHalo halo_reverse_send(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, const char* slot) {
   const size_t gp = size_t(acc.G) * s.plane();
   std::string base(slot);
-  float* top = static_cast<float*>(workspace(ctx, base + "_rtop", gp * sizeof(float)));
-  float* bot = static_cast<float*>(workspace(ctx, base + "_rbot", gp * sizeof(float)));
+  RevHalo r;
+  r.top = static_cast<float*>(workspace(ctx, base + "_rtop", gp * sizeof(float)));
+  r.bot = static_cast<float*>(workspace(ctx, base + "_rbot", gp * sizeof(float)));
+  r.G = acc.G;
   const int p = ctx->nranks;
   const int prev = (ctx->rank - 1 + p) % p, next = (ctx->rank + 1) % p;
-  {
-    Timed t(ctx, T_SCATTER_COMM);
-    VB_NCCL(ncclGroupStart());
-    VB_NCCL(ncclSend(acc.lo, gp, ncclFloat, prev, ctx->comm, ctx->stream));
-    VB_NCCL(ncclSend(acc.hi, gp, ncclFloat, next, ctx->comm, ctx->stream));
-    VB_NCCL(ncclRecv(top, gp, ncclFloat, next, ctx->comm, ctx->stream));
-    VB_NCCL(ncclRecv(bot, gp, ncclFloat, prev, ctx->comm, ctx->stream));
-    VB_NCCL(ncclGroupEnd());
-  }
+  Timed t(ctx, T_SCATTER_COMM);
+  VB_NCCL(ncclGroupStart());
+  VB_NCCL(ncclSend(acc.lo, gp, ncclFloat, prev, ctx->comm, ctx->stream));
+  VB_NCCL(ncclSend(acc.hi, gp, ncclFloat, next, ctx->comm, ctx->stream));
+  VB_NCCL(ncclRecv(r.top, gp, ncclFloat, next, ctx->comm, ctx->stream));
+  VB_NCCL(ncclRecv(r.bot, gp, ncclFloat, prev, ctx->comm, ctx->stream));
+  VB_NCCL(ncclGroupEnd());
   ctx->comm_bytes[C_SCATTER_POINTS] += 2 * gp * sizeof(float);
   ctx->comm_bytes[C_P2P_MSGS] += 2;
+  return r;
+}
+
+void halo_reverse_finish(vreg_ctx ctx, const Slab& s, const RevHalo& r, float* out) {
+  const size_t gp = size_t(r.G) * s.plane();
   Timed t(ctx, T_SCATTER_BUF);
   k_add_planes<<<blocks_for(gp, 256), 256, 0, ctx->stream>>>(
-      gp, top, out + size_t(s.n1l - acc.G) * s.plane());
-  k_add_planes<<<blocks_for(gp, 256), 256, 0, ctx->stream>>>(gp, bot, out);
+      gp, r.top, out + size_t(s.n1l - r.G) * s.plane());
+  k_add_planes<<<blocks_for(gp, 256), 256, 0, ctx->stream>>>(gp, r.bot, out);
   count_launch(ctx, 2);
   check_launch();
+}
+
+void halo_reverse_add(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, float* out,
+                      const char* slot) {
+  halo_reverse_finish(ctx, s, halo_reverse_send(ctx, s, acc, slot), out);
 }
 
 int sl_ghost_width(vreg_ctx ctx, const Slab& s, const float* disp1, int degree) {

@@ -299,7 +299,7 @@ __device__ __forceinline__ float tile_gather(const Geo& g, const SrcField<DIST>&
 // Point `it` of this thread in the tile (warp w: rows it*8 + w; lanes: x3).
 #define TILE_PT(it)                                                          \
   const int row_##it = (it) * (TILE_THREADS / 32) + (threadIdx.x >> 5);      \
-  const int i = blockIdx.z * TT1 + row_##it / TT2;                           \
+  const int i = layer * TT1 + row_##it / TT2;                                \
   const int j = blockIdx.y * TT2 + row_##it % TT2;                           \
   const int k = blockIdx.x * TT3 + (threadIdx.x & 31);                       \
   const bool ok = i < g.n1l && j < g.n2 && k < g.n3;                         \
@@ -311,10 +311,11 @@ template <int DEG, bool DIST, int MODE>  // MODE 0: interp(*q), 1: inc-state ste
 __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_gather_tile(
     Geo g, SrcField<DIST> src, const int* __restrict__ boxes, const float* __restrict__ D,
     const float* __restrict__ qf, float* __restrict__ out, const float* __restrict__ vt,
-    const float* __restrict__ gr, float half, int last, float* __restrict__ mt_out) {
+    const float* __restrict__ gr, float half, int last, float* __restrict__ mt_out, TileZ zm) {
   extern __shared__ __align__(16) float fbox[];
   __shared__ const float* rows[BOX_ROWS_MAX];
-  const TileBox b = load_tile_box(boxes, tile_index());
+  const int layer = tile_layer(zm);
+  const TileBox b = load_tile_box(boxes, tile_index_at(layer, int(gridDim.y)));
   const bool fits = b.ext[0] > 0;
   if (fits) {  // uniform per CTA
     if (box_vec(g)) {
@@ -365,11 +366,13 @@ template <int DEG, bool DIST>
 __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_scatter_tile(Geo g, DstField<DIST> dst,
                                                                   const int* __restrict__ boxes,
                                                                   const float* __restrict__ D,
-                                                                  const float* __restrict__ z) {
+                                                                  const float* __restrict__ z,
+                                                                  TileZ lay) {
   extern __shared__ __align__(16) int ibox[];
   __shared__ unsigned s_zmax;
   __shared__ float* rows[BOX_ROWS_MAX];
-  const TileBox b = load_tile_box(boxes, tile_index());
+  const int layer = tile_layer(lay);
+  const TileBox b = load_tile_box(boxes, tile_index_at(layer, int(gridDim.y)));
   const bool fits = b.ext[0] > 0;
   if (threadIdx.x == 0) s_zmax = 0u;
   if (fits) {
@@ -417,6 +420,99 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_scatter_tile(
 inline dim3 tile_grid(const Slab& s) {
   return dim3(unsigned((s.n3 + TT3 - 1) / TT3), unsigned((s.n2 + TT2 - 1) / TT2),
               unsigned((s.n1l + TT1 - 1) / TT1));
+}
+
+constexpr TileZ kAllLayers{0, 1 << 30, 0};
+
+inline dim3 tile_grid_nz(const Slab& s, int nz) {
+  dim3 g = tile_grid(s);
+  g.z = unsigned(nz);
+  return g;
+}
+
+// x1 tile layers of a slab whose stencils stay clear of the ghost planes for
+// ghost width G (floor(max|d1|) + 3): layer z reaches planes
+// [4z - G + 1, 4z + G + 2], so zb = ceil((G + 3) / 4) boundary layers per side.
+struct LayerSplit {
+  bool on = false;
+  int zb = 0, ntz = 0;
+};
+inline LayerSplit layer_split(const Slab& s, int G) {
+  LayerSplit l;
+  l.ntz = (s.n1l + TT1 - 1) / TT1;
+  l.zb = (G + 3 + TT1 - 1) / TT1;
+  static const bool overlap = [] {
+    const char* e = std::getenv("VREG_HALO_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
+  l.on = overlap && 2 * l.zb < l.ntz;
+  return l;
+}
+
+struct OnStream {  // issue on another stream for the scope (NCCL + its timers)
+  vreg_ctx c;
+  cudaStream_t prev;
+  OnStream(vreg_ctx c_, cudaStream_t st) : c(c_), prev(c_->stream) { c->stream = st; }
+  ~OnStream() { c->stream = prev; }
+};
+
+// Tile gather on several ranks: the halo exchange of f runs on the comm
+// stream while the interior layers (no ghost reads) run; the two boundary
+// bands follow once the ghosts have landed. launch(TileZ, nz) issues the
+// tile kernel on ctx->stream.
+template <class Launch>
+void gather_tiles(vreg_ctx ctx, const Slab& s, const float* f, int G, bool dist, Ghosts& gh,
+                  Launch launch) {
+  const LayerSplit ls = layer_split(s, dist ? G : 0);
+  if (!dist) {
+    launch(kAllLayers, ls.ntz);
+    return;
+  }
+  if (!ls.on) {
+    gh = halo_exchange(ctx, s, f, G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
+    launch(kAllLayers, ls.ntz);
+    return;
+  }
+  VB_CUDA(cudaEventRecord(ctx->ev_c0, ctx->stream));
+  VB_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_c0, 0));
+  {
+    OnStream os(ctx, ctx->comm_stream);
+    gh = halo_exchange(ctx, s, f, G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
+    VB_CUDA(cudaEventRecord(ctx->ev_c1, ctx->stream));
+  }
+  launch(TileZ{ls.zb, 1 << 30, 0}, ls.ntz - 2 * ls.zb);
+  VB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_c1, 0));
+  launch(TileZ{0, ls.zb, ls.ntz - ls.zb}, 2 * ls.zb);
+}
+
+// Tile scatter on several ranks: the boundary bands (the only tiles that
+// write ghost accumulators) go first, their reverse exchange overlaps the
+// interior layers, and the received planes are added at the end.
+template <class Launch>
+void scatter_tiles(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, float* out, bool dist,
+                   Launch launch) {
+  const LayerSplit ls = layer_split(s, dist ? acc.G : 0);
+  if (!dist) {
+    launch(kAllLayers, ls.ntz);
+    return;
+  }
+  if (!ls.on) {
+    launch(kAllLayers, ls.ntz);
+    halo_reverse_add(ctx, s, acc, out, "sl_gacc");
+    return;
+  }
+  launch(TileZ{0, ls.zb, ls.ntz - ls.zb}, 2 * ls.zb);
+  VB_CUDA(cudaEventRecord(ctx->ev_c0, ctx->stream));
+  VB_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_c0, 0));
+  RevHalo r;
+  {
+    OnStream os(ctx, ctx->comm_stream);
+    r = halo_reverse_send(ctx, s, acc, "sl_gacc");
+    VB_CUDA(cudaEventRecord(ctx->ev_c1, ctx->stream));
+  }
+  launch(TileZ{ls.zb, 1 << 30, 0}, ls.ntz - 2 * ls.zb);
+  VB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_c1, 0));
+  halo_reverse_finish(ctx, s, r, out);
 }
 
 // Box table of the characteristics disp3 (cached per pointer/grid/degree;
@@ -597,18 +693,20 @@ void interp_sweep(vreg_ctx ctx, const Slab& s, const float* f, const float* disp
   }
   const bool dist = ctx->nranks > 1;
   Ghosts gh;
-  if (dist) gh = halo_exchange(ctx, s, f, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
+  if (dist && !use_tile())
+    gh = halo_exchange(ctx, s, f, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
   Timed t(ctx, T_SL, "sl_interp");
   const Geo g = geo_of(s);
   const dim3 grid = sl_grid(s), block(BX, BY);
   if (use_tile()) {
     const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
-    const int* boxes = tl.boxes;
-    SL_DISPATCH(degree, dist,
-                (tile_kernel(k_gather_tile<DEG, DIST, 0>)<<<tile_grid(s), TILE_THREADS,
-                                                             tl.smem, ctx->stream>>>(
-                    g, src_of<DIST>(f, gh), boxes, disp3, q, out, nullptr, nullptr, 0.f, 0,
-                    nullptr)));
+    gather_tiles(ctx, s, f, ci.G, dist, gh, [&](TileZ zm, int nz) {
+      SL_DISPATCH(degree, dist,
+                  (tile_kernel(k_gather_tile<DEG, DIST, 0>)<<<tile_grid_nz(s, nz), TILE_THREADS,
+                                                               tl.smem, ctx->stream>>>(
+                      g, src_of<DIST>(f, gh), tl.boxes, disp3, q, out, nullptr, nullptr, 0.f, 0,
+                      nullptr, zm)));
+    });
   }
   else if (use_quad(s))
     SL_DISPATCH(degree, dist,
@@ -644,11 +742,13 @@ void scatter_sweep(vreg_ctx ctx, const Slab& s, const float* z, const float* dis
     const dim3 grid = sl_grid(s), block(BX, BY);
     if (use_tile()) {
       const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
-    const int* boxes = tl.boxes;
-      SL_DISPATCH(degree, dist,
-                  (tile_kernel(k_scatter_tile<DEG, DIST>)<<<tile_grid(s), TILE_THREADS, tl.smem,
-                                               ctx->stream>>>(g, dst_of<DIST>(out, acc), boxes,
-                                                              disp3, z)));
+      scatter_tiles(ctx, s, acc, out, dist, [&](TileZ zm, int nz) {
+        SL_DISPATCH(degree, dist,
+                    (tile_kernel(k_scatter_tile<DEG, DIST>)<<<tile_grid_nz(s, nz), TILE_THREADS,
+                                                              tl.smem, ctx->stream>>>(
+                        g, dst_of<DIST>(out, acc), tl.boxes, disp3, z, zm)));
+      });
+      return;
     }
     else if (use_quad(s))
       SL_DISPATCH(degree, dist,
@@ -711,23 +811,27 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
     float* wn = last ? psi_out : w + size_t((t + 1) & 1) * N;
     float* mo = mt_all ? mt_all + size_t(t + 1) * N : nullptr;
     Ghosts gh;
-    if (dist) gh = halo_exchange(ctx, s, wt, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
+    if (dist && !use_tile())
+      gh = halo_exchange(ctx, s, wt, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
     Timed tm(ctx, T_SL, "sl_inc_step");
     if (fused_u) {
       const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
-      SL_DISPATCH(degree, dist,
-                  (tile_kernel(k_gather_tile<DEG, DIST, 2>)<<<tile_grid(s), TILE_THREADS,
-                                                               tl.smem, ctx->stream>>>(
-                      g, src_of<DIST>(wt, gh), tl.boxes, disp3, u + size_t(t) * N, wn, nullptr,
-                      nullptr, half, last ? 1 : 0, mo)));
+      gather_tiles(ctx, s, wt, ci.G, dist, gh, [&](TileZ zm, int nz) {
+        SL_DISPATCH(degree, dist,
+                    (tile_kernel(k_gather_tile<DEG, DIST, 2>)<<<tile_grid_nz(s, nz), TILE_THREADS,
+                                                                 tl.smem, ctx->stream>>>(
+                        g, src_of<DIST>(wt, gh), tl.boxes, disp3, u + size_t(t) * N, wn, nullptr,
+                        nullptr, half, last ? 1 : 0, mo, zm)));
+      });
     } else if (use_tile() && !ci.identity) {
       const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
-    const int* boxes = tl.boxes;
-      SL_DISPATCH(degree, dist,
-                  (tile_kernel(k_gather_tile<DEG, DIST, 1>)<<<tile_grid(s), TILE_THREADS,
-                                                               tl.smem, ctx->stream>>>(
-                      g, src_of<DIST>(wt, gh), boxes, disp3, nullptr, wn, vt3,
-                      grads + size_t(t + 1) * 3 * N, half, last ? 1 : 0, mo)));
+      gather_tiles(ctx, s, wt, ci.G, dist, gh, [&](TileZ zm, int nz) {
+        SL_DISPATCH(degree, dist,
+                    (tile_kernel(k_gather_tile<DEG, DIST, 1>)<<<tile_grid_nz(s, nz), TILE_THREADS,
+                                                                 tl.smem, ctx->stream>>>(
+                        g, src_of<DIST>(wt, gh), tl.boxes, disp3, nullptr, wn, vt3,
+                        grads + size_t(t + 1) * 3 * N, half, last ? 1 : 0, mo, zm)));
+      });
     }
     else if (use_quad(s))
       SL_DISPATCH(degree, dist,

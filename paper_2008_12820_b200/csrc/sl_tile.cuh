@@ -67,6 +67,21 @@ __device__ __forceinline__ int tile_index() {
   return (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
 }
 
+// x1 tile-layer range of a launch: layer = z < zs ? z0 + z : z1 + (z - zs).
+// Full launches use {0, INT_MAX, 0}; on several ranks the interior layers
+// (boxes clear of the ghost planes) and the two boundary bands are launched
+// separately so the halo exchange overlaps the interior tiles.
+struct TileZ {
+  int z0, zs, z1;
+};
+__device__ __forceinline__ int tile_layer(const TileZ& m) {
+  const int z = int(blockIdx.z);
+  return z < m.zs ? m.z0 + z : m.z1 + (z - m.zs);
+}
+__device__ __forceinline__ int tile_index_at(int layer, int ntile_y) {
+  return (layer * ntile_y + int(blockIdx.y)) * int(gridDim.x) + int(blockIdx.x);
+}
+
 // Point (i, j, k) of iteration `it` of this thread: warp w covers rows
 // (x1, x2) = (it*8 + w) / TT2, % TT2 and its lanes the 32 x3 columns.
 #define TILE_POINT_LOOP(g)                                                     \

@@ -276,7 +276,7 @@ void launch_axis(vreg_ctx ctx, const AxisGeom& s, int n, const float* v3, float*
   check_launch();
 }
 
-// x1-slab [c][i1l][j][k] -> per-peer blocks [q][c][i1l][j_l][k] (j = q n2l + j_l)
+// x1-slab [c][i1l][j][k] -> blocks [c][q][i1l][j_l][k] (j = q n2l + j_l)
 __global__ void k_axis_pack(int p, int n1l, int n2l, int n3, const float4* __restrict__ in,
                             float4* __restrict__ out) {
   const int n34 = n3 / 4;
@@ -291,11 +291,11 @@ __global__ void k_axis_pack(int p, int n1l, int n2l, int n3, const float4* __res
     const int j = int(r % (size_t(p) * n2l));
     const int i = int(r / (size_t(p) * n2l));
     const int q = j / n2l, jl = j - q * n2l;
-    out[((((size_t(q) * 3 + c) * n1l + i) * n2l + jl) * n34) + k4] = in[e];
+    out[((((size_t(c) * p + q) * n1l + i) * n2l + jl) * n34) + k4] = in[e];
   }
 }
 
-// out3[c][i1l][j][k] += blocks[q][c][i1l][j_l][k]
+// out3[c][i1l][j][k] += blocks[c][q][i1l][j_l][k]
 __global__ void k_axis_unpack_add(int p, int n1l, int n2l, int n3, const float4* __restrict__ in,
                                   float4* __restrict__ out) {
   const int n34 = n3 / 4;
@@ -310,7 +310,7 @@ __global__ void k_axis_unpack_add(int p, int n1l, int n2l, int n3, const float4*
     const int j = int(r % (size_t(p) * n2l));
     const int i = int(r / (size_t(p) * n2l));
     const int q = j / n2l, jl = j - q * n2l;
-    const float4 a = in[((((size_t(q) * 3 + c) * n1l + i) * n2l + jl) * n34) + k4];
+    const float4 a = in[((((size_t(c) * p + q) * n1l + i) * n2l + jl) * n34) + k4];
     float4 o = out[e];
     o.x += a.x;
     o.y += a.y;
@@ -320,24 +320,96 @@ __global__ void k_axis_unpack_add(int p, int n1l, int n2l, int n3, const float4*
   }
 }
 
-// Grouped send/recv of per-(peer, component) blocks of `blk` floats.
-// send_off / recv_off give each block's offset (in floats) for peer q, comp c.
-template <class SendOff, class RecvOff>
-void axis_exchange(vreg_ctx ctx, const float* send, float* recv, size_t blk, SendOff so,
-                   RecvOff ro) {
-  const int p = ctx->nranks;
-  VB_NCCL(ncclGroupStart());
-  for (int q = 0; q < p; ++q) {
-    if (q == ctx->rank) continue;
-    for (int c = 0; c < 3; ++c) {
-      VB_NCCL(ncclSend(send + so(q, c), blk, ncclFloat, q, ctx->comm, ctx->stream));
-      VB_NCCL(ncclRecv(recv + ro(q, c), blk, ncclFloat, q, ctx->comm, ctx->stream));
-    }
+// Transpose buffers. Peer path: cudaMalloc'd send/recv buffers whose
+// receive side is opened by every peer through CUDA IPC (handles all-gathered
+// over NCCL; collective, every rank arrives with the same size).
+bool axis_buffers(vreg_ctx ctx, size_t bytes, float** a, float** b) {
+  static const bool peer = [] {
+    const char* e = std::getenv("VREG_PEER_TRANSPOSE");
+    return !(e && e[0] == '0');
+  }();
+  if (!peer) {
+    *a = static_cast<float*>(workspace(ctx, "axis_a", bytes));
+    *b = static_cast<float*>(workspace(ctx, "axis_b", bytes));
+    return false;
   }
-  VB_NCCL(ncclGroupEnd());
+  if (ctx->xbytes < bytes) {
+    VB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (float* q : ctx->peer_recv)
+      if (q) VB_CUDA(cudaIpcCloseMemHandle(q));
+    ctx->peer_recv.clear();
+    for (int i = 0; i < 2; ++i)
+      if (ctx->xbuf[i]) VB_CUDA(cudaFree(ctx->xbuf[i]));
+    for (int i = 0; i < 2; ++i) VB_CUDA(cudaMalloc(&ctx->xbuf[i], bytes));
+    if (!ctx->xflag) VB_CUDA(cudaMalloc(&ctx->xflag, 64 * sizeof(int)));
+    const int p = ctx->nranks;
+    cudaIpcMemHandle_t h;
+    VB_CUDA(cudaIpcGetMemHandle(&h, ctx->xbuf[1]));
+    char* dh = nullptr;
+    VB_CUDA(cudaMalloc(&dh, size_t(p + 1) * sizeof(h)));
+    VB_CUDA(cudaMemcpyAsync(dh + size_t(p) * sizeof(h), &h, sizeof(h), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    VB_NCCL(ncclAllGather(dh + size_t(p) * sizeof(h), dh, sizeof(h), ncclChar, ctx->comm,
+                          ctx->stream));
+    std::vector<cudaIpcMemHandle_t> all(p);
+    VB_CUDA(cudaMemcpyAsync(all.data(), dh, size_t(p) * sizeof(h), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    VB_CUDA(cudaStreamSynchronize(ctx->stream));
+    VB_CUDA(cudaFree(dh));
+    ctx->peer_recv.assign(p, nullptr);
+    for (int q = 0; q < p; ++q) {
+      if (q == ctx->rank) continue;
+      void* ptr = nullptr;
+      VB_CUDA(cudaIpcOpenMemHandle(&ptr, all[q], cudaIpcMemLazyEnablePeerAccess));
+      ctx->peer_recv[q] = static_cast<float*>(ptr);
+    }
+    ctx->xbytes = bytes;
+  }
+  *a = ctx->xbuf[0];
+  *b = ctx->xbuf[1];
+  return true;
+}
+
+// Stream-ordered barrier across ranks (a 1-int all-reduce): on return every
+// rank's earlier work on its stream is complete.
+void axis_barrier(vreg_ctx ctx) {
+  VB_NCCL(ncclAllReduce(ctx->xflag, ctx->xflag + 32, 1, ncclInt, ncclSum, ctx->comm,
+                        ctx->stream));
+}
+
+// All-to-all of [c][q] blocks of `blk` floats, one per component: block
+// (c, q) of `send` goes to rank q and lands at block (c, me) of its `recv`.
+// Peer path: the copy engines write straight into the peers' receive buffers
+// over NVLink (no SM time taken from the SL sweeps), bracketed by barriers
+// (peers done reading the previous contents / all blocks landed).
+void axis_alltoall(vreg_ctx ctx, const float* send, float* recv, size_t blk, bool peer) {
+  const int p = ctx->nranks, me = ctx->rank;
+  if (peer) {
+    axis_barrier(ctx);
+    for (int k = 1; k < p; ++k) {
+      const int q = (me + k) % p;  // stagger the targets
+      for (int c = 0; c < 3; ++c)
+        VB_CUDA(cudaMemcpyAsync(ctx->peer_recv[q] + (size_t(c) * p + me) * blk,
+                                send + (size_t(c) * p + q) * blk, blk * sizeof(float),
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+  } else {
+    VB_NCCL(ncclGroupStart());
+    for (int q = 0; q < p; ++q) {
+      if (q == me) continue;
+      for (int c = 0; c < 3; ++c) {
+        VB_NCCL(ncclSend(send + (size_t(c) * p + q) * blk, blk, ncclFloat, q, ctx->comm,
+                         ctx->stream));
+        VB_NCCL(ncclRecv(recv + (size_t(c) * p + q) * blk, blk, ncclFloat, q, ctx->comm,
+                         ctx->stream));
+      }
+    }
+    VB_NCCL(ncclGroupEnd());
+  }
   for (int c = 0; c < 3; ++c)
-    VB_CUDA(cudaMemcpyAsync(recv + ro(ctx->rank, c), send + so(ctx->rank, c), blk * sizeof(float),
-                            cudaMemcpyDeviceToDevice, ctx->stream));
+    VB_CUDA(cudaMemcpyAsync(recv + (size_t(c) * p + me) * blk, send + (size_t(c) * p + me) * blk,
+                            blk * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (peer) axis_barrier(ctx);
   ctx->comm_bytes[C_FFT_TRANSPOSE] += uint64_t(p - 1) * 3 * blk * sizeof(float);
   ctx->comm_bytes[C_ALLTOALL] += 1;
 }
@@ -351,26 +423,21 @@ void dist_axis1(vreg_ctx ctx, const Slab& s, const float* v3, float* out3, doubl
   const int p = ctx->nranks, n1l = s.n1l, n2l = s.n2 / p, n3 = s.n3;
   const size_t blk = size_t(n1l) * n2l * n3;  // floats per (peer, component)
   const size_t all = 3 * size_t(p) * blk;
-  float* a = static_cast<float*>(workspace(ctx, "axis_a", all * sizeof(float)));
-  float* b = static_cast<float*>(workspace(ctx, "axis_b", all * sizeof(float)));
+  float *a, *b;
+  const bool ce = axis_buffers(ctx, all * sizeof(float), &a, &b);
   const unsigned g4 = unsigned(blocks_for(all / 4, 256));
   k_axis_pack<<<g4, 256, 0, ctx->stream>>>(p, n1l, n2l, n3, reinterpret_cast<const float4*>(v3),
                                            reinterpret_cast<float4*>(a));
   count_launch(ctx);
   check_launch();
-  const size_t comp_x2 = size_t(s.n1) * n2l * n3;  // one component in the x2-slab layout
-  {
+  {  // b[c] = component c on the x2 slab, [i1 = q n1l + i1l][j_l][k]
     Timed t(ctx, T_TRANSPOSE);
-    axis_exchange(
-        ctx, a, b, blk, [&](int q, int c) { return (size_t(q) * 3 + c) * blk; },
-        [&](int q, int c) { return size_t(c) * comp_x2 + size_t(q) * blk; });
+    axis_alltoall(ctx, a, b, blk, ce);
   }
   launch_axis<1>(ctx, AxisGeom{s.n1, n2l, n3}, s.n1, b, a, beta, 0, cap);
   {
     Timed t(ctx, T_TRANSPOSE);
-    axis_exchange(
-        ctx, a, b, blk, [&](int q, int c) { return size_t(c) * comp_x2 + size_t(q) * blk; },
-        [&](int q, int c) { return (size_t(q) * 3 + c) * blk; });
+    axis_alltoall(ctx, a, b, blk, ce);
   }
   k_axis_unpack_add<<<g4, 256, 0, ctx->stream>>>(p, n1l, n2l, n3,
                                                  reinterpret_cast<const float4*>(b),
