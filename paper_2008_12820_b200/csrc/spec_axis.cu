@@ -97,6 +97,15 @@ __device__ __forceinline__ void dft(float2 (&a)[R]) {
 
 constexpr int AX_THREADS = 256;
 
+// Pencil decomposition N = T1 * R2: T1 threads per complex pencil, NP
+// complex (2 NP real) pencils per CTA; 1024-point pencils use 32 threads so
+// a thread still holds 32 values.
+template <int N>
+struct AxisShape {
+  static constexpr int T1 = N <= 512 ? 16 : 32;
+  static constexpr int NP = AX_THREADS / T1;
+};
+
 // out (+)= coef * D_ax v over all 3 components. coef = beta / N (1-D
 // inverse normalisation folded in); tw[m] = exp(-2 pi i m / N). CTAs walk
 // the (component, tile) list with a grid stride: one tile each when the grid
@@ -109,28 +118,31 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 2) k_axis_d2(int n1
                                                          float* __restrict__ out,
                                                          const float2* __restrict__ tw,
                                                          float coef, int accumulate) {
-  constexpr int R2 = N / 16;
-  constexpr int SK = 17, SP = R2 * SK + 1;  // odd float2 pitches: conflict-free
-  extern __shared__ float2 S[];  // 16 * SP
+  constexpr int T1 = AxisShape<N>::T1, NP = AxisShape<N>::NP, WQ = 2 * NP;
+  constexpr int R2 = N / T1;
+  constexpr int SK = T1 + 1, SP = R2 * SK + 1;  // odd float2 pitches: conflict-free
+  extern __shared__ float2 S[];  // NP * SP
   const size_t nloc = size_t(n1l) * n2 * n3;
   for (int t = blockIdx.x; t < 3 * tiles; t += gridDim.x) {
   const int comp = t / tiles, tile = t - comp * tiles;
   const float* vc = v + size_t(comp) * nloc;
   float* oc = out + size_t(comp) * nloc;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  // x3 pass: half-warps run along a row (n1 fastest); x2/x1 passes: along
-  // the 16 column pairs of a 128-byte row (p fastest)
-  const int n1 = AX == 3 ? (l & 15) : 2 * w + (l >> 4);
-  const int p = AX == 3 ? 2 * w + (l >> 4) : (l & 15);
+  (void)w;
+  (void)l;
+  // x3 pass: T1 lanes run along a row (n1 fastest); x2/x1 passes: along the
+  // NP column pairs of a row segment (p fastest)
+  const int n1 = AX == 3 ? int(threadIdx.x) % T1 : int(threadIdx.x) / NP;
+  const int p = AX == 3 ? int(threadIdx.x) / T1 : int(threadIdx.x) % NP;
   size_t base, js, qs;
   if constexpr (AX == 3) {
-    base = size_t(tile) * 32 * n3;
+    base = size_t(tile) * WQ * n3;
     js = 1;
     qs = size_t(n3);
   } else {
-    const int nb = n3 / 32;
+    const int nb = n3 / WQ;
     const int r = tile / nb, xb = tile - r * nb;
-    base = (AX == 2 ? size_t(r) * n2 * n3 : size_t(r) * n3) + size_t(xb) * 32;
+    base = (AX == 2 ? size_t(r) * n2 * n3 : size_t(r) * n3) + size_t(xb) * WQ;
     js = AX == 2 ? size_t(n3) : size_t(n2) * n3;
     qs = 1;
   }
@@ -139,7 +151,7 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 2) k_axis_d2(int n1
   if (accumulate) {  // pull the output rows towards L2 while v streams in
 #pragma unroll
     for (int m = 0; m < R2; ++m) {
-      const float* q = oc + off + size_t(16 * m) * js;
+      const float* q = oc + off + size_t(T1 * m) * js;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
       if constexpr (AX == 3) asm volatile("prefetch.global.L2 [%0];" ::"l"(q + qs));
     }
@@ -147,7 +159,7 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 2) k_axis_d2(int n1
   float2 a[R2];
 #pragma unroll
   for (int m = 0; m < R2; ++m) {
-    const float* q = vc + off + size_t(16 * m) * js;
+    const float* q = vc + off + size_t(T1 * m) * js;
     if constexpr (AX == 3)
       a[m] = make_float2(__ldg(q), __ldg(q + qs));
     else
@@ -161,22 +173,22 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 2) k_axis_d2(int n1
     Sp[k2 * SK + n1] = a[k2];
   }
   __syncthreads();
-  for (int k2 = n1; k2 < R2; k2 += 16) {  // 16-point DFTs over n1, symbol, inverse
-    float2 b[16];
+  for (int k2 = n1; k2 < R2; k2 += T1) {  // T1-point DFTs over n1, symbol, inverse
+    float2 b[T1];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) b[j] = Sp[k2 * SK + j];
-    dft<16, -1>(b);
+    for (int j = 0; j < T1; ++j) b[j] = Sp[k2 * SK + j];
+    dft<T1, -1>(b);
 #pragma unroll
-    for (int k1 = 0; k1 < 16; ++k1) {
+    for (int k1 = 0; k1 < T1; ++k1) {
       const int f = k2 + R2 * k1;
       const float fs = float(f <= N / 2 ? f : f - N);
       const float m = coef * fs * fs;
       b[k1].x *= m;
       b[k1].y *= m;
     }
-    dft<16, 1>(b);
+    dft<T1, 1>(b);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) Sp[k2 * SK + j] = b[j];
+    for (int j = 0; j < T1; ++j) Sp[k2 * SK + j] = b[j];
   }
   __syncthreads();
 #pragma unroll
@@ -187,7 +199,7 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 2) k_axis_d2(int n1
   dft<R2, 1>(a);
 #pragma unroll
   for (int m = 0; m < R2; ++m) {
-    float* q = oc + off + size_t(16 * m) * js;
+    float* q = oc + off + size_t(T1 * m) * js;
     if constexpr (AX == 3) {
       if (accumulate) {
         q[0] += a[m].x;
@@ -210,7 +222,7 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 2) k_axis_d2(int n1
   }
 }
 
-bool axis_size_ok(int n) { return n >= 32 && n <= 512 && (n & (n - 1)) == 0; }
+bool axis_size_ok(int n) { return n >= 32 && n <= 1024 && (n & (n - 1)) == 0; }
 
 const float2* twiddles(vreg_ctx ctx, int n) {
   const std::string name = "axis_tw_" + std::to_string(n);
@@ -236,8 +248,9 @@ struct AxisGeom {
 template <int AX>
 void launch_axis(vreg_ctx ctx, const AxisGeom& s, int n, const float* v3, float* out3,
                  double beta, int accumulate, int ctas_per_sm) {
-  const int tiles = AX == 3 ? int(size_t(s.n1l) * s.n2 / 32)
-                            : (AX == 2 ? s.n1l : s.n2) * (s.n3 / 32);
+  const int wq = n <= 512 ? 32 : 16;  // 2 * AxisShape<n>::NP
+  const int tiles = AX == 3 ? int(size_t(s.n1l) * s.n2 / wq)
+                            : (AX == 2 ? s.n1l : s.n2) * (s.n3 / wq);
   static const char* names[4] = {"", "spec_axis1", "spec_axis2", "spec_axis3"};
   Timed timer(ctx, T_FFT, names[AX]);
   int grid = 3 * tiles;
@@ -251,7 +264,8 @@ void launch_axis(vreg_ctx ctx, const AxisGeom& s, int n, const float* v3, float*
   const float coef = float(beta / double(n));
 #define VB_AXIS_CASE(NN)                                                                   \
   case NN: {                                                                               \
-    const size_t smem = size_t(16) * ((NN / 16) * 17 + 1) * sizeof(float2);               \
+    const size_t smem = size_t(AxisShape<NN>::NP) *                                        \
+                        ((NN / AxisShape<NN>::T1) * (AxisShape<NN>::T1 + 1) + 1) * sizeof(float2); \
     static const bool attr = [&] {                                                         \
       VB_CUDA(cudaFuncSetAttribute(k_axis_d2<NN, AX>,                                      \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); \
@@ -268,6 +282,7 @@ void launch_axis(vreg_ctx ctx, const AxisGeom& s, int n, const float* v3, float*
     VB_AXIS_CASE(128)
     VB_AXIS_CASE(256)
     VB_AXIS_CASE(512)
+    VB_AXIS_CASE(1024)
     default:
       require(false, VREG_EDIM, "axis transform size");
   }

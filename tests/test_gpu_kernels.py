@@ -118,7 +118,7 @@ def test_fd_nonsquare_and_constant(ctx):
     assert float(ctx.fd_grad(g, c).abs().max()) == 0.0  # paired form: exact (test_fd.cpp:72-78)
 
 
-@pytest.mark.parametrize("shape", [(32, 32, 32), (64, 32, 128), (32, 256, 64), (512, 32, 32)])
+@pytest.mark.parametrize("shape", [(32, 32, 32), (64, 32, 128), (32, 256, 64), (512, 32, 32), (1024, 32, 32), (32, 32, 1024)])
 def test_regop_separable_passes(ctx, shape):
     """Zero-null-mode regop runs as three 1-D spectral passes (spec_axis.cu)
     on power-of-two grids; white noise exercises every mode incl. Nyquist.
