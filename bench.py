@@ -277,23 +277,33 @@ def run_ours(args):
     ms = float(t.item())
     value = Nvox * args.steps / (ms * 1e-3) / 1e6
 
-    # ---- e2e: the public API with HOST buffers, copies inside the timed region
-    h_in = torch.empty(vt.shape, dtype=torch.float32, pin_memory=True)
-    h_in.copy_(vt)
-    h_out = torch.empty(vt.shape, dtype=torch.float32, pin_memory=True)
+    # ---- e2e: the public API with HOST buffers, copies inside the timed region.
+    # vreg_solver_matvec_host_async pipelines call k's upload, call k-1's
+    # matvec and call k-2's download (PCIe is full duplex); every step's
+    # H2D of its input and D2H of its result is inside the timed region,
+    # which is host wall clock between full device synchronisations.
+    h_in = [torch.empty(vt.shape, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    for h in h_in:
+        h.copy_(vt)
+    h_out = [torch.empty(vt.shape, dtype=torch.float32, pin_memory=True) for _ in range(2)]
 
-    def step_e2e():  # vreg_solver_matvec_host: H2D, fused matvec, D2H
-        solver.matvec_host(h_in, h_out)
+    def run_e2e(k):
+        for i in range(k):
+            solver.matvec_host_async(h_in[i % 2], h_out[i % 2])
+        solver.wait()
 
-    for _ in range(2):
-        step_e2e()
+    run_e2e(2)
+    torch.cuda.synchronize()
     barrier()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step_e2e()
-    ev1.record(stream)
+    t0 = time.perf_counter()
+    run_e2e(args.steps)
+    torch.cuda.synchronize()
+    ms_e2e = (time.perf_counter() - t0) * 1e3
     barrier()
-    ms_e2e = ev0.elapsed_time(ev1)
+    # the pipelined result equals the blocking call's
+    ref_out = torch.empty_like(h_out[0])
+    solver.matvec_host(h_in[0], ref_out)
+    e2e_diff = float((ref_out - h_out[(args.steps - 1) % 2]).norm() / ref_out.norm())
     t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -398,7 +408,9 @@ def run_ours(args):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes,
-                    "d2h_bytes_per_step": nbytes, "ms_per_step": ms_e2e / args.steps},
+                    "d2h_bytes_per_step": nbytes, "ms_per_step": ms_e2e / args.steps,
+                    "api": "vreg_solver_matvec_host_async (pinned host buffers, 2 slots)",
+                    "rel_diff_vs_blocking_call": e2e_diff},
             "gpu_launches": launches,
             "sl_tiles": dict(zip(("built", "over_smem_budget"), ctx.tile_stats())),
             "clocks": clk.summary(),

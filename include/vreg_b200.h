@@ -61,6 +61,15 @@ int vreg_solver_gradient(vreg_solver s, float* g3);
 int vreg_solver_matvec(vreg_solver s, const float* vt3, float* out3);
 /* the same matvec on HOST buffers (H2D + matvec + D2H) */
 int vreg_solver_matvec_host(vreg_solver s, const float* vt3_host, float* out3_host);
+
+/* Pipelined host-buffer matvec: enqueue H2D of vt3_host, the fused matvec
+ * and D2H into out3_host, and return. Two device slots and two copy streams
+ * (H2D, D2H) let call k's upload, call k-1's matvec and call k-2's download
+ * overlap. Both host buffers must be pinned and stay untouched until
+ * vreg_solver_wait returns. Same result as vreg_solver_matvec_host. */
+int vreg_solver_matvec_host_async(vreg_solver s, const float* vt3_host, float* out3_host);
+/* Block until every enqueued host-buffer matvec has landed in host memory. */
+int vreg_solver_wait(vreg_solver s);
 /* stats4: inva applications, h0 applications, inner iterations, capped */
 int vreg_solver_precond(vreg_solver s, int kind, const float* r3, double eps_k, float* out3,
                         uint64_t stats4[4]);

@@ -62,6 +62,8 @@ int vreg_ctx_create_dist(int device, int rank, int nranks, const void* uid128,
                          vreg_ctx* out);
 int vreg_ctx_destroy(vreg_ctx ctx);
 int vreg_ctx_rank(vreg_ctx ctx, int* rank, int* nranks);
+/* The stream all calls on ctx are ordered on (cudaStream_t). */
+int vreg_ctx_get_stream(vreg_ctx ctx, void** stream);
 int vreg_ctx_set_stream(vreg_ctx ctx, void* cuda_stream);
 void* vreg_ctx_stream(vreg_ctx ctx);
 int vreg_ctx_synchronize(vreg_ctx ctx);

@@ -270,6 +270,13 @@ int vreg_ctx_rank(vreg_ctx ctx, int* rank, int* nranks) {
   return VREG_OK;
 }
 
+int vreg_ctx_get_stream(vreg_ctx ctx, void** s) {
+  return guard([&] {
+    require(s != nullptr, VREG_EPARAM, "null argument");
+    *s = ctx->stream;
+  });
+}
+
 int vreg_ctx_set_stream(vreg_ctx ctx, void* s) {
   return guard([&] {
     VB_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -1,9 +1,11 @@
 // Solver-level C ABI (include/vreg_b200.h) over the C++ host layer
 // (include/vreg_b200/solver.hpp). Exceptions never cross the ABI: they map
 // back to the status codes of vreg_cuda.h.
+#include <cuda_runtime.h>
 #include <cstring>
 #include <memory>
 #include <optional>
+#include <stdexcept>
 #include <string>
 
 #include "vreg_b200.h"
@@ -26,6 +28,25 @@ struct vreg_solver_s {
   Real beta = 0;
   std::unique_ptr<Preconditioner> prec;
   std::optional<DVField> io_in, io_out;  // device staging of the host-buffer matvec
+  // pipelined host-buffer matvec: two slots, upload / download streams
+  std::optional<DVField> pin[2], pout[2];
+  cudaStream_t up = nullptr, down = nullptr;
+  cudaEvent_t ev_up[2] = {}, ev_mv[2] = {}, ev_down[2] = {};
+  bool slot_used[2] = {false, false};
+  std::uint64_t pk = 0;
+  ~vreg_solver_s() {
+    if (up) {
+      cudaStreamSynchronize(up);
+      cudaStreamSynchronize(down);
+      cudaStreamDestroy(up);
+      cudaStreamDestroy(down);
+      for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(ev_up[i]);
+        cudaEventDestroy(ev_mv[i]);
+        cudaEventDestroy(ev_down[i]);
+      }
+    }
+  }
 };
 
 namespace {
@@ -265,6 +286,60 @@ int vreg_solver_matvec_host(vreg_solver s, const float* vt3_host, float* out3_ho
     if (!direct_matvec(s, s->io_in->data(), s->io_out->data()))
       *s->io_out = hessian_matvec(e, *s->lin, *s->io_in, s->beta, s->cfg);
     check(vreg_memcpy_d2h(e.ctx(), out3_host, s->io_out->data(), bytes));
+  });
+}
+
+namespace {
+void cuda_check(cudaError_t e) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+}
+}  // namespace
+
+int vreg_solver_matvec_host_async(vreg_solver s, const float* vt3_host, float* out3_host) {
+  return guarded([&] {
+    require_lin(s);
+    CudaEngine& e = s->eng;
+    void* mv = nullptr;
+    check(vreg_ctx_get_stream(e.ctx(), &mv));
+    cudaStream_t st = static_cast<cudaStream_t>(mv);
+    if (!s->up) {
+      cuda_check(cudaStreamCreateWithFlags(&s->up, cudaStreamNonBlocking));
+      cuda_check(cudaStreamCreateWithFlags(&s->down, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        cuda_check(cudaEventCreateWithFlags(&s->ev_up[i], cudaEventDisableTiming));
+        cuda_check(cudaEventCreateWithFlags(&s->ev_mv[i], cudaEventDisableTiming));
+        cuda_check(cudaEventCreateWithFlags(&s->ev_down[i], cudaEventDisableTiming));
+        s->pin[i].emplace(e.make_vfield());
+        s->pout[i].emplace(e.make_vfield());
+      }
+      cuda_check(cudaStreamSynchronize(st));  // slots allocated on the matvec stream
+    }
+    const int k = int(s->pk & 1);
+    const size_t bytes = 3 * s->pin[k]->local_points() * sizeof(float);
+    // upload into slot k once call k-2's matvec has consumed it
+    if (s->slot_used[k]) cuda_check(cudaStreamWaitEvent(s->up, s->ev_mv[k], 0));
+    cuda_check(cudaMemcpyAsync(s->pin[k]->data(), vt3_host, bytes, cudaMemcpyHostToDevice, s->up));
+    cuda_check(cudaEventRecord(s->ev_up[k], s->up));
+    // matvec once the upload landed and call k-2's download freed the output
+    cuda_check(cudaStreamWaitEvent(st, s->ev_up[k], 0));
+    if (s->slot_used[k]) cuda_check(cudaStreamWaitEvent(st, s->ev_down[k], 0));
+    if (!direct_matvec(s, s->pin[k]->data(), s->pout[k]->data()))
+      *s->pout[k] = hessian_matvec(e, *s->lin, *s->pin[k], s->beta, s->cfg);
+    cuda_check(cudaEventRecord(s->ev_mv[k], st));
+    cuda_check(cudaStreamWaitEvent(s->down, s->ev_mv[k], 0));
+    cuda_check(cudaMemcpyAsync(out3_host, s->pout[k]->data(), bytes, cudaMemcpyDeviceToHost,
+                               s->down));
+    cuda_check(cudaEventRecord(s->ev_down[k], s->down));
+    s->slot_used[k] = true;
+    ++s->pk;
+  });
+}
+
+int vreg_solver_wait(vreg_solver s) {
+  return guarded([&] {
+    if (!s->up) return;
+    cuda_check(cudaStreamSynchronize(s->up));
+    cuda_check(cudaStreamSynchronize(s->down));
   });
 }
 

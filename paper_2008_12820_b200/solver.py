@@ -91,6 +91,8 @@ _SOLVER_SIGS = {
     "vreg_solver_gradient": (C.c_int, [C.c_void_p, C.c_void_p]),
     "vreg_solver_matvec": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "vreg_solver_matvec_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vreg_solver_matvec_host_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vreg_solver_wait": (C.c_int, [C.c_void_p]),
     "vreg_solver_precond": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_double, C.c_void_p,
                                       C.POINTER(C.c_uint64)]),
     "vreg_solver_register": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_double),
@@ -167,6 +169,18 @@ class Solver:
         check(lib().vreg_solver_matvec_host(self.h, C.c_void_p(vt_host.data_ptr()),
                                             C.c_void_p(out_host.data_ptr())))
         return out_host
+
+    def matvec_host_async(self, vt_host, out_host):
+        """Enqueue the host-buffer matvec (pinned float32 tensors) and return;
+        consecutive calls overlap upload, matvec and download. Buffers stay
+        owned by the caller until wait()."""
+        assert vt_host.device.type == "cpu" and vt_host.is_pinned() and out_host.is_pinned()
+        check(lib().vreg_solver_matvec_host_async(self.h, C.c_void_p(vt_host.data_ptr()),
+                                                  C.c_void_p(out_host.data_ptr())))
+        return out_host
+
+    def wait(self):
+        check(lib().vreg_solver_wait(self.h))
 
     def precond(self, kind, r, eps_k):
         out = self.field(3)

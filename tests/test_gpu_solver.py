@@ -83,6 +83,14 @@ def test_matvec_host_buffers(lin64):
     h_out = torch.empty_like(h_in).pin_memory()
     s.matvec_host(h_in, h_out)
     assert rel(h_out.double().numpy(), d) < 1e-6
+    # pipelined variant: 5 calls over 2 slots with distinct inputs
+    ins = [(vt * (1 + 0.25 * i)).cpu().pin_memory() for i in range(5)]
+    outs = [torch.empty_like(h_in).pin_memory() for _ in range(5)]
+    for a, b in zip(ins, outs):
+        s.matvec_host_async(a, b)
+    s.wait()
+    for i, b in enumerate(outs):  # the matvec is linear in vt
+        assert rel(b.double().numpy(), (1 + 0.25 * i) * d) < 1e-6
 
 
 @pytest.mark.parametrize("kind", ["inva", "invh0", "2linvh0"])
