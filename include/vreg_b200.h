@@ -77,6 +77,20 @@ int vreg_solver_precond(vreg_solver s, int kind, const float* r3, double eps_k, 
  * final_g_rel, total_gn, total_pcg, flagged, phases pc/obj/grad/hess/total,
  * kernels fft/fd/sl, levels. counters21 in KernelCounters order. */
 int vreg_solver_register(vreg_solver s, float* v_out3, double rep16[16], uint64_t counters21[21]);
+/* Text of the last vreg_solver_register report (include/vreg_b200/report.hpp):
+ * which 0 = render_report (deterministic, no timings), 1 = render_timings,
+ * 2 = render_residuals_csv (reference report.hpp:79-84). Copies at most cap-1
+ * bytes + NUL into buf; *len = full length. */
+int vreg_solver_report_text(vreg_solver s, int which, char* buf, size_t cap, size_t* len);
+
+/* VolumeFile "VRG1", host buffers: kind 0 = f32, 1 = f64;
+ * ncomp 1 or 3; data = components concatenated, row-major. Bad magic or a
+ * payload length that disagrees with the header -> VREG_EIO. */
+int vreg_volume_save(const char* path, int n1, int n2, int n3, int kind, int ncomp,
+                     const void* data);
+int vreg_volume_header(const char* path, int hdr5[5]); /* n1, n2, n3, kind, ncomp */
+int vreg_volume_load(const char* path, void* data, size_t cap_bytes);
+
 int vreg_solver_counters(vreg_solver s, uint64_t counters21[21]);
 int vreg_solver_reset_counters(vreg_solver s);
 

@@ -62,6 +62,10 @@ int vreg_ctx_create_dist(int device, int rank, int nranks, const void* uid128,
                          vreg_ctx* out);
 int vreg_ctx_destroy(vreg_ctx ctx);
 int vreg_ctx_rank(vreg_ctx ctx, int* rank, int* nranks);
+/* Transpose (scatter) sweeps in exact fixed point: bitwise reproducible and
+ * independent of the GPU count, ~10% slower matvec. Default off (fp32 L2
+ * reductions, run-to-run differences in the last bits); env VREG_DETERMINISTIC=1. */
+int vreg_ctx_set_deterministic(vreg_ctx ctx, int on);
 /* The stream all calls on ctx are ordered on (cudaStream_t). */
 int vreg_ctx_get_stream(vreg_ctx ctx, void** stream);
 int vreg_ctx_set_stream(vreg_ctx ctx, void* cuda_stream);

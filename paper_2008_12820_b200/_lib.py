@@ -32,6 +32,11 @@ _SIGS = {
     "vreg_ctx_destroy": (I, [VP]),
     "vreg_ctx_rank": (I, [VP, C.POINTER(I), C.POINTER(I)]),
     "vreg_ctx_set_stream": (I, [VP, VP]),
+    "vreg_ctx_get_stream": (I, [VP, C.POINTER(VP)]),
+    "vreg_ctx_set_deterministic": (I, [VP, I]),
+    "vreg_volume_save": (I, [C.c_char_p, I, I, I, I, I, VP]),
+    "vreg_volume_header": (I, [C.c_char_p, C.POINTER(I)]),
+    "vreg_volume_load": (I, [C.c_char_p, VP, C.c_size_t]),
     "vreg_ctx_stream": (VP, [VP]),
     "vreg_ctx_synchronize": (I, [VP]),
     "vreg_slab": (I, [VP, GP, C.POINTER(I), C.POINTER(I)]),

@@ -122,6 +122,9 @@ struct vreg_ctx_s {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // halo exchanges of the distributed SL sweeps run here, overlapping the
   // interior tiles (high priority so NCCL's CTAs are scheduled promptly)
+  // transpose sweeps in exact fixed point (bitwise reproducible, independent
+  // of the GPU count) instead of fp32 L2 reductions (VREG_DETERMINISTIC=1)
+  bool deterministic = false;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;
   // regulariser x2-slab transposes by copy engine into the peers' buffers
@@ -250,9 +253,10 @@ struct RevHalo {
   int G = 0;
 };
 RevHalo halo_reverse_send(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, const char* slot);
-void halo_reverse_finish(vreg_ctx ctx, const Slab& s, const RevHalo& r, float* out);
+void halo_reverse_finish(vreg_ctx ctx, const Slab& s, const RevHalo& r, float* out,
+                         bool as_int = false);
 void halo_reverse_add(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, float* out,
-                      const char* slot);
+                      const char* slot, bool as_int = false);
 // Ghost width for a semi-Lagrangian sweep: floor(max|disp1|) + degree-dependent
 // stencil reach; checked against the slab width.
 int sl_ghost_width(vreg_ctx ctx, const Slab& s, const float* disp1, int degree);

@@ -162,6 +162,10 @@ int vreg_status_exit_code(int status) {
 }
 
 static void init_ctx(vreg_ctx c, int device) {
+  {
+    const char* e = std::getenv("VREG_DETERMINISTIC");
+    c->deterministic = e && e[0] == '1';
+  }
   c->device = device;
   VB_CUDA(cudaSetDevice(device));
   VB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -268,6 +272,10 @@ int vreg_ctx_rank(vreg_ctx ctx, int* rank, int* nranks) {
   if (rank) *rank = ctx->rank;
   if (nranks) *nranks = ctx->nranks;
   return VREG_OK;
+}
+
+int vreg_ctx_set_deterministic(vreg_ctx ctx, int on) {
+  return guard([&] { ctx->deterministic = on != 0; });
 }
 
 int vreg_ctx_get_stream(vreg_ctx ctx, void** s) {

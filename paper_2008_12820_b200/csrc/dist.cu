@@ -22,6 +22,20 @@ __global__ void k_add_planes(size_t n, const float* __restrict__ src, float* __r
     dst[i] += src[i];
 }
 
+// fixed-point accumulators (int32, or packed int64 pairs when n3 % 4 == 0,
+// see fixed_add) stored in the float buffers
+__global__ void k_add_planes_int(size_t n, const int* __restrict__ src, int* __restrict__ dst) {
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] += src[i];
+}
+__global__ void k_add_planes_i64(size_t n2, const long long* __restrict__ src,
+                                 long long* __restrict__ dst) {
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n2; i += stride)
+    dst[i] += src[i];
+}
+
 // received [q][k2l][c*n1l + il][h]  ->  F[c][q*n1l + il][k2l][h]
 __global__ void k_unpack(int p, int ncomp, int n1l, int n2l, int h, const float2* __restrict__ in,
                          float2* __restrict__ out) {
@@ -180,9 +194,30 @@ RevHalo halo_reverse_send(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, cons
   return r;
 }
 
-void halo_reverse_finish(vreg_ctx ctx, const Slab& s, const RevHalo& r, float* out) {
+void halo_reverse_finish(vreg_ctx ctx, const Slab& s, const RevHalo& r, float* out,
+                         bool as_int) {
   const size_t gp = size_t(r.G) * s.plane();
   Timed t(ctx, T_SCATTER_BUF);
+  if (as_int && s.n3 % 4 == 0) {  // packed pairs
+    k_add_planes_i64<<<blocks_for(gp / 2, 256), 256, 0, ctx->stream>>>(
+        gp / 2, reinterpret_cast<const long long*>(r.top),
+        reinterpret_cast<long long*>(out + size_t(s.n1l - r.G) * s.plane()));
+    k_add_planes_i64<<<blocks_for(gp / 2, 256), 256, 0, ctx->stream>>>(
+        gp / 2, reinterpret_cast<const long long*>(r.bot), reinterpret_cast<long long*>(out));
+    count_launch(ctx, 2);
+    check_launch();
+    return;
+  }
+  if (as_int) {
+    k_add_planes_int<<<blocks_for(gp, 256), 256, 0, ctx->stream>>>(
+        gp, reinterpret_cast<const int*>(r.top),
+        reinterpret_cast<int*>(out + size_t(s.n1l - r.G) * s.plane()));
+    k_add_planes_int<<<blocks_for(gp, 256), 256, 0, ctx->stream>>>(
+        gp, reinterpret_cast<const int*>(r.bot), reinterpret_cast<int*>(out));
+    count_launch(ctx, 2);
+    check_launch();
+    return;
+  }
   k_add_planes<<<blocks_for(gp, 256), 256, 0, ctx->stream>>>(
       gp, r.top, out + size_t(s.n1l - r.G) * s.plane());
   k_add_planes<<<blocks_for(gp, 256), 256, 0, ctx->stream>>>(gp, r.bot, out);
@@ -191,8 +226,8 @@ void halo_reverse_finish(vreg_ctx ctx, const Slab& s, const RevHalo& r, float* o
 }
 
 void halo_reverse_add(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, float* out,
-                      const char* slot) {
-  halo_reverse_finish(ctx, s, halo_reverse_send(ctx, s, acc, slot), out);
+                      const char* slot, bool as_int) {
+  halo_reverse_finish(ctx, s, halo_reverse_send(ctx, s, acc, slot), out, as_int);
 }
 
 int sl_ghost_width(vreg_ctx ctx, const Slab& s, const float* disp1, int degree) {

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "vreg_b200.h"
+#include "vreg_b200/report.hpp"
 #include "vreg_b200/solver.hpp"
 
 namespace vb {
@@ -28,6 +29,7 @@ struct vreg_solver_s {
   Real beta = 0;
   std::unique_ptr<Preconditioner> prec;
   std::optional<DVField> io_in, io_out;  // device staging of the host-buffer matvec
+  std::optional<SolverReport> last;      // of the last vreg_solver_register
   // pipelined host-buffer matvec: two slots, upload / download streams
   std::optional<DVField> pin[2], pout[2];
   cudaStream_t up = nullptr, down = nullptr;
@@ -373,6 +375,7 @@ int vreg_solver_register(vreg_solver s, float* v_out3, double rep16[16], uint64_
     CudaEngine& e = s->eng;
     DVField v;
     SolverReport r = register_images(e, s->m0, s->m1, s->cfg, &v);
+    s->last = r;
     if (v_out3)
       check(vreg_memcpy_d2d(e.ctx(), v_out3, v.data(), 3 * v.local_points() * sizeof(float)));
     if (rep16) {
@@ -394,6 +397,58 @@ int vreg_solver_register(vreg_solver s, float* v_out3, double rep16[16], uint64_
       rep16[15] = double(r.levels.size());
     }
     if (counters21) dump_counters(r.counters, counters21);
+  });
+}
+
+int vreg_solver_report_text(vreg_solver s, int which, char* buf, size_t cap, size_t* len) {
+  return guarded([&] {
+    if (!s->last) throw config_error("no registration report yet (call vreg_solver_register)");
+    const std::string t = which == 0   ? render_report(*s->last)
+                          : which == 1 ? render_timings(*s->last)
+                          : which == 2 ? render_residuals_csv(*s->last)
+                                       : throw parameter_error("report kind must be 0, 1 or 2");
+    if (len) *len = t.size();
+    if (buf && cap) {
+      const size_t n = t.size() < cap - 1 ? t.size() : cap - 1;
+      std::memcpy(buf, t.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+
+int vreg_volume_save(const char* path, int n1, int n2, int n3, int kind, int ncomp,
+                     const void* data) {
+  return guarded([&] {
+    Volume v;
+    v.n1 = n1;
+    v.n2 = n2;
+    v.n3 = n3;
+    v.kind = kind;
+    v.ncomp = ncomp;
+    if ((kind != 0 && kind != 1) || (ncomp != 1 && ncomp != 3) || n1 <= 0 || n2 <= 0 || n3 <= 0)
+      throw parameter_error("volume: bad header fields");
+    const auto* p = static_cast<const unsigned char*>(data);
+    v.payload.assign(p, p + v.expected_bytes());
+    save_volume(path, v);
+  });
+}
+
+int vreg_volume_header(const char* path, int hdr5[5]) {
+  return guarded([&] {
+    const Volume v = load_volume(path);
+    hdr5[0] = v.n1;
+    hdr5[1] = v.n2;
+    hdr5[2] = v.n3;
+    hdr5[3] = v.kind;
+    hdr5[4] = v.ncomp;
+  });
+}
+
+int vreg_volume_load(const char* path, void* data, size_t cap_bytes) {
+  return guarded([&] {
+    const Volume v = load_volume(path);
+    if (cap_bytes < v.payload.size()) throw parameter_error("volume: destination too small");
+    std::memcpy(data, v.payload.data(), v.payload.size());
   });
 }
 

@@ -362,8 +362,13 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_gather_tile(
   }
 }
 
+// Default transpose sweep: per-tile power-of-two scale S = 2^(27-e_tile)
+// in the shared int32 box (exact to 2^-28 max|z_tile| per contribution),
+// flushed with float4 REDs. The L2 adds of overlapping tiles land in any
+// order, so the last bits can differ between runs (VREG_DETERMINISTIC=1 /
+// vreg_ctx_set_deterministic selects the fixed-point variant below).
 template <int DEG, bool DIST>
-__global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_scatter_tile(Geo g, DstField<DIST> dst,
+__global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_scatter_tile_fp(Geo g, DstField<DIST> dst,
                                                                   const int* __restrict__ boxes,
                                                                   const float* __restrict__ D,
                                                                   const float* __restrict__ z,
@@ -416,6 +421,117 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_scatter_tile(
     flush_box(g, dst, b, ibox, invS, rows);
   }
 }
+
+// Transpose sweep into an int32 accumulator field at the sweep's global
+// fixed-point scale S = 2^(26 - e), max|z| < 2^e (zmax_bits: device, the max
+// over all ranks). Every contribution is rounded once (DFMA), tiles add
+// integers (shared then global atomics), so the result is exact in its
+// quantisation and independent of tile / rank order: bitwise reproducible.
+// A cell holds up to 32 max|z|; each contribution is exact to 2^-27 max|z|.
+template <int DEG, bool DIST>
+__global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_scatter_tile(Geo g, DstField<DIST> dst,
+                                                                  const int* __restrict__ boxes,
+                                                                  const float* __restrict__ D,
+                                                                  const float* __restrict__ z,
+                                                                  const unsigned* __restrict__ zmax_bits,
+                                                                  TileZ lay) {
+  extern __shared__ __align__(16) int ibox[];
+  __shared__ float* rows[BOX_ROWS_MAX];
+  const unsigned zmb = __ldg(zmax_bits);
+  if (zmb == 0u) return;  // z == 0 everywhere: the (zeroed) output stays 0
+  const int layer = tile_layer(lay);
+  const TileBox b = load_tile_box(boxes, tile_index_at(layer, int(gridDim.y)));
+  const bool fits = b.ext[0] > 0;
+  if (fits) {
+    if (box_vec(g)) box_rows<DIST>(g, dst, b, rows);  // read after the barriers below
+    const int words = b.ext[0] * b.ext[1] * BOX_PITCH;
+    int4* ib4 = reinterpret_cast<int4*>(ibox);  // words % 64 == 0
+    for (int c = threadIdx.x; c < words / 4; c += TILE_THREADS) ib4[c] = make_int4(0, 0, 0, 0);
+  }
+  float zv[TILE_PPT], d1[TILE_PPT], d2[TILE_PPT], d3[TILE_PPT];
+#pragma unroll
+  for (int it = 0; it < TILE_PPT; ++it) {
+    TILE_PT(it)
+    zv[it] = ok ? z[p] : 0.f;
+    d1[it] = ok ? D[p] : 0.f;
+    d2[it] = ok ? D[g.N + p] : 0.f;
+    d3[it] = ok ? D[2 * g.N + p] : 0.f;
+  }
+  float invS;
+  const float S = fixed_scale(zmb, &invS);
+  __syncthreads();  // box zeroed, row table written
+#pragma unroll
+  for (int it = 0; it < TILE_PPT; ++it) {
+    TILE_PT(it)
+    if (!ok || zv[it] == 0.0f) continue;
+    BoxStencil<DEG> bs;
+    if (fits && bs.build(b, i, j, k, d1[it], d2[it], d3[it]))
+      bs.scatter(b, ibox, zv[it] * S);
+    else
+      point_scatter_fixed<DEG, DIST>(g, dst, i, j, k, d1[it], d2[it], d3[it], zv[it] * S);
+  }
+  if (fits) {
+    __syncthreads();
+    flush_box_fixed(g, dst, b, ibox, rows);
+  }
+}
+
+// block max -> one atomic per CTA (blockDim.x == 256)
+__device__ __forceinline__ void block_max_atomic(unsigned m, unsigned* out) {
+  __shared__ unsigned sm[8];
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < 8 ? sm[threadIdx.x] : 0u;
+    m = __reduce_max_sync(0xffffffffu, m);
+    if (threadIdx.x == 0 && m) atomicMax(out, m);
+  }
+}
+
+// max |x| over n floats as float bits (non-negative floats order as uints)
+__global__ void k_maxabs_bits(size_t n, const float* __restrict__ x, unsigned* __restrict__ out) {
+  unsigned m = 0u;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    m = max(m, __float_as_uint(fabsf(x[i])));
+  block_max_atomic(m, out);
+}
+
+// packed pairs (n % 4 == 0): two int64 words = four cells per thread-iteration
+__global__ void k_fixed_finish(size_t n4, const longlong2* __restrict__ I,
+                               const unsigned* __restrict__ zmax_bits, float4* __restrict__ out,
+                               unsigned* __restrict__ next_max) {
+  float inv;
+  fixed_scale(__ldg(zmax_bits), &inv);
+  unsigned m = 0u;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const longlong2 v = I[i];
+    const int a = int(v.x), c = int(v.y);  // low halves, sign-extended
+    const int b = int((v.x - a) >> 32), d = int((v.y - c) >> 32);
+    const float4 f = make_float4(float(a) * inv, float(b) * inv, float(c) * inv, float(d) * inv);
+    out[i] = f;
+    m = max(max(max(m, __float_as_uint(fabsf(f.x))), __float_as_uint(fabsf(f.y))),
+            max(__float_as_uint(fabsf(f.z)), __float_as_uint(fabsf(f.w))));
+  }
+  if (next_max) block_max_atomic(m, next_max);
+}
+
+__global__ void k_fixed_finish1(size_t n, const int* __restrict__ I,
+                                const unsigned* __restrict__ zmax_bits, float* __restrict__ out,
+                                unsigned* __restrict__ next_max) {
+  float inv;
+  fixed_scale(__ldg(zmax_bits), &inv);
+  unsigned m = 0u;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    out[i] = float(I[i]) * inv;
+    m = max(m, __float_as_uint(fabsf(out[i])));
+  }
+  if (next_max) block_max_atomic(m, next_max);
+}
+
 
 inline dim3 tile_grid(const Slab& s) {
   return dim3(unsigned((s.n3 + TT3 - 1) / TT3), unsigned((s.n2 + TT2 - 1) / TT2),
@@ -490,7 +606,7 @@ void gather_tiles(vreg_ctx ctx, const Slab& s, const float* f, int G, bool dist,
 // interior layers, and the received planes are added at the end.
 template <class Launch>
 void scatter_tiles(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, float* out, bool dist,
-                   Launch launch) {
+                   Launch launch, bool as_int = false) {
   const LayerSplit ls = layer_split(s, dist ? acc.G : 0);
   if (!dist) {
     launch(kAllLayers, ls.ntz);
@@ -498,7 +614,7 @@ void scatter_tiles(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, float* out,
   }
   if (!ls.on) {
     launch(kAllLayers, ls.ntz);
-    halo_reverse_add(ctx, s, acc, out, "sl_gacc");
+    halo_reverse_add(ctx, s, acc, out, "sl_gacc", as_int);
     return;
   }
   launch(TileZ{0, ls.zb, ls.ntz - ls.zb}, 2 * ls.zb);
@@ -512,7 +628,7 @@ void scatter_tiles(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, float* out,
   }
   launch(TileZ{ls.zb, 1 << 30, 0}, ls.ntz - 2 * ls.zb);
   VB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_c1, 0));
-  halo_reverse_finish(ctx, s, r, out);
+  halo_reverse_finish(ctx, s, r, out, as_int);
 }
 
 // Box table of the characteristics disp3 (cached per pointer/grid/degree;
@@ -723,43 +839,93 @@ void interp_sweep(vreg_ctx ctx, const Slab& s, const float* f, const float* disp
 }
 
 // out = I^T z (out is overwritten)
+// out = I^T z (out is overwritten). Tile path: deterministic fixed point
+// (k_scatter_tile); zmax = device max|z| bits of this sweep's input (computed
+// here when null), next_max (optional) receives max|out| bits for a
+// following sweep. The per-point fallback paths (VREG_SL_TILE=0) use fp32
+// atomics.
 void scatter_sweep(vreg_ctx ctx, const Slab& s, const float* z, const float* disp3,
-                   const CharsInfo& ci, int degree, float* out) {
+                   const CharsInfo& ci, int degree, float* out, unsigned* zmax = nullptr,
+                   unsigned* next_max = nullptr) {
+  const size_t N = s.local();
   if (ci.identity) {
     if (out != z)
-      VB_CUDA(cudaMemcpyAsync(out, z, s.local() * sizeof(float), cudaMemcpyDeviceToDevice,
+      VB_CUDA(cudaMemcpyAsync(out, z, N * sizeof(float), cudaMemcpyDeviceToDevice,
                               ctx->stream));
+    if (next_max) {
+      k_maxabs_bits<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, out, next_max);
+      count_launch(ctx);
+      check_launch();
+    }
     return;
   }
   require(out != z, VREG_EPARAM, "scatter cannot run in place");
   const bool dist = ctx->nranks > 1;
   GhostAcc acc;
   if (dist) acc = ghost_accumulators(ctx, s, ci.G, "sl_gacc");
-  {
-    Timed t(ctx, T_SL, "sl_scatter_sweep");
-    VB_CUDA(cudaMemsetAsync(out, 0, s.local() * sizeof(float), ctx->stream));
-    const Geo g = geo_of(s);
-    const dim3 grid = sl_grid(s), block(BX, BY);
-    if (use_tile()) {
-      const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
-      scatter_tiles(ctx, s, acc, out, dist, [&](TileZ zm, int nz) {
-        SL_DISPATCH(degree, dist,
-                    (tile_kernel(k_scatter_tile<DEG, DIST>)<<<tile_grid_nz(s, nz), TILE_THREADS,
-                                                              tl.smem, ctx->stream>>>(
-                        g, dst_of<DIST>(out, acc), tl.boxes, disp3, z, zm)));
-      });
-      return;
-    }
-    else if (use_quad(s))
+  Timed t(ctx, T_SL, "sl_scatter_sweep");
+  const Geo g = geo_of(s);
+  const dim3 grid = sl_grid(s), block(BX, BY);
+  if (use_tile() && !ctx->deterministic) {
+    VB_CUDA(cudaMemsetAsync(out, 0, N * sizeof(float), ctx->stream));
+    const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
+    scatter_tiles(ctx, s, acc, out, dist, [&](TileZ zm, int nz) {
       SL_DISPATCH(degree, dist,
-                  (k_scatter_q<DEG, DIST><<<slq_grid(s), block, 0, ctx->stream>>>(
-                      g, dst_of<DIST>(out, acc), disp3, z)));
-    else
-      SL_DISPATCH(degree, dist,
-                  (k_scatter<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
-                      g, dst_of<DIST>(out, acc), disp3, z)));
+                  (tile_kernel(k_scatter_tile_fp<DEG, DIST>)<<<tile_grid_nz(s, nz), TILE_THREADS,
+                                                               tl.smem, ctx->stream>>>(
+                      g, dst_of<DIST>(out, acc), tl.boxes, disp3, z, zm)));
+    });
+    return;
   }
+  if (use_tile()) {
+    if (!zmax) {
+      zmax = static_cast<unsigned*>(workspace(ctx, "sc_zmax", 64));
+      VB_CUDA(cudaMemsetAsync(zmax, 0, sizeof(unsigned), ctx->stream));
+      k_maxabs_bits<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, z, zmax);
+      count_launch(ctx);
+      check_launch();
+    }
+    if (dist)  // one scale on every rank
+      VB_NCCL(ncclAllReduce(zmax, zmax, 1, ncclUint32, ncclMax, ctx->comm, ctx->stream));
+    float* I = static_cast<float*>(workspace(ctx, "sc_fixed", N * sizeof(float)));  // int32
+    VB_CUDA(cudaMemsetAsync(I, 0, N * sizeof(float), ctx->stream));
+    const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
+    scatter_tiles(
+        ctx, s, acc, I, dist,
+        [&](TileZ zm, int nz) {
+          SL_DISPATCH(degree, dist,
+                      (tile_kernel(k_scatter_tile<DEG, DIST>)<<<tile_grid_nz(s, nz), TILE_THREADS,
+                                                                tl.smem, ctx->stream>>>(
+                          g, dst_of<DIST>(I, acc), tl.boxes, disp3, z, zmax, zm)));
+        },
+        true);
+    if (s.n3 % 4 == 0) {  // packed pairs (fixed_add)
+      k_fixed_finish<<<blocks_for(N / 4, 256), 256, 0, ctx->stream>>>(
+          N / 4, reinterpret_cast<const longlong2*>(I), zmax, reinterpret_cast<float4*>(out),
+          next_max);
+    } else {
+      k_fixed_finish1<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(
+          N, reinterpret_cast<const int*>(I), zmax, out, next_max);
+    }
+    count_launch(ctx);
+    check_launch();
+    return;
+  }
+  VB_CUDA(cudaMemsetAsync(out, 0, N * sizeof(float), ctx->stream));
+  if (use_quad(s))
+    SL_DISPATCH(degree, dist,
+                (k_scatter_q<DEG, DIST><<<slq_grid(s), block, 0, ctx->stream>>>(
+                    g, dst_of<DIST>(out, acc), disp3, z)));
+  else
+    SL_DISPATCH(degree, dist,
+                (k_scatter<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
+                    g, dst_of<DIST>(out, acc), disp3, z)));
   if (dist) halo_reverse_add(ctx, s, acc, out, "sl_gacc");
+  if (next_max) {
+    k_maxabs_bits<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, out, next_max);
+    count_launch(ctx);
+    check_launch();
+  }
 }
 
 }  // namespace
@@ -852,8 +1018,19 @@ void sl_transpose_sweeps(vreg_ctx ctx, const Slab& s, const float* disp3, int fl
   check_degree(degree);
   const CharsInfo ci = chars_info(ctx, s, disp3, flags, degree);
   const size_t N = s.local();
+  // max|psi_t| bits per slice: each sweep's finish hands the next its scale
+  unsigned* mx = nullptr;
+  if (ctx->deterministic && use_tile() && !ci.identity) {
+    mx = static_cast<unsigned*>(workspace(ctx, "sc_chain", 64 * sizeof(unsigned)));
+    VB_CUDA(cudaMemsetAsync(mx, 0, size_t(s.nt + 1) * sizeof(unsigned), ctx->stream));
+    k_maxabs_bits<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, psi + size_t(s.nt) * N,
+                                                               mx + s.nt);
+    count_launch(ctx);
+    check_launch();
+  }
   for (int t = s.nt; t > 0; --t)
-    scatter_sweep(ctx, s, psi + size_t(t) * N, disp3, ci, degree, psi + size_t(t - 1) * N);
+    scatter_sweep(ctx, s, psi + size_t(t) * N, disp3, ci, degree, psi + size_t(t - 1) * N,
+                  mx ? mx + t : nullptr, mx && t > 1 ? mx + t - 1 : nullptr);
 }
 
 void sl_assemble(vreg_ctx ctx, const Slab& s, int descending, const float* sl,

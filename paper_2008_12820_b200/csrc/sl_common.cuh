@@ -23,6 +23,23 @@ struct Geo {
   size_t N;      // local points
 };
 
+// One fixed-point contribution into an int32 accumulator field. Packed mode
+// (n3 % 4 == 0): adjacent cells (2m, 2m+1) share one 64-bit word updated as
+// lo + 2^32 hi -- exact in int64, decoded per pair once every cell's total
+// fits int32 -- so the tile flush needs half the atomics. Every writer of a
+// field must use the same mode.
+__device__ __forceinline__ void fixed_add(int* p, int v, bool packed) {
+  if (packed) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    unsigned long long* q = reinterpret_cast<unsigned long long*>(a & ~uintptr_t(7));
+    const long long w = (a & 4) ? (static_cast<long long>(v) << 32) : static_cast<long long>(v);
+    atomicAdd(q, static_cast<unsigned long long>(w));
+  } else {
+    atomicAdd(p, v);
+  }
+}
+__device__ __forceinline__ bool fixed_packed(const Geo& g) { return (g.n3 & 3) == 0; }
+
 __device__ __forceinline__ void split_axis(float d, int q, int& base, float& s) {
   const float fd = floorf(d);
   s = d - fd;  // exact in fp32
@@ -164,6 +181,36 @@ struct Stencil {
       }
     }
   }
+
+  // Fixed-point variant: dst holds int32 at scale S (zS = z S); each
+  // contribution rounded as the tile path does (DFMA against 1.5 * 2^52).
+  template <bool DIST>
+  __device__ __forceinline__ void scatter_fixed(const Geo& g, const DstField<DIST>& dst,
+                                                float zS) const {
+    constexpr double MAGIC = 6755399441055744.0;
+#pragma unroll
+    for (int a = 0; a < NN; ++a) {
+      int* P = reinterpret_cast<int*>(dst.plane_ptr(p1[a], g));
+      const float za = w1[a] * zS;
+#pragma unroll
+      for (int b = 0; b < NN; ++b) {
+        int* R = P + r2[b];
+        const double zab = double(za * w2[b]);
+#pragma unroll
+        for (int c = 0; c < NN; ++c)
+          fixed_add(R + c3[c], __double2loint(fma(zab, double(w3[c]), MAGIC)), fixed_packed(g));
+      }
+    }
+  }
 };
+
+// Global fixed-point scale of a transpose sweep: S = 2^(26 - e) with
+// max|z| < 2^e, from the max's float bits (device memory, uniform).
+__device__ __forceinline__ float fixed_scale(unsigned zmax_bits, float* inv) {
+  int e = 0;
+  frexpf(__uint_as_float(zmax_bits), &e);
+  *inv = ldexpf(1.0f, e - 26);
+  return ldexpf(1.0f, 26 - e);
+}
 
 }  // namespace vb

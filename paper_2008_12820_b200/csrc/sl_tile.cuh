@@ -275,6 +275,48 @@ __device__ __forceinline__ void flush_box(const Geo& g, const DstField<DIST>& ds
   }
 }
 
+// Integer flush: the box (int32 at the sweep's global scale) is added into
+// the int32 accumulator field with integer atomics -- exact, so the result
+// does not depend on the order tiles (or ranks) arrive in.
+template <bool DIST>
+__device__ __forceinline__ void flush_box_fixed(const Geo& g, const DstField<DIST>& dst,
+                                                const TileBox& b, const int* sbox,
+                                                float* const* rows) {
+  if (box_vec(g)) {
+    const int q = threadIdx.x & 15;
+    if (4 * q < b.ext[2]) {
+      const int c = wrap_once(b.lo[2] + 4 * q, g.n3);
+      const int nr = b.ext[0] * b.ext[1];
+      for (int r = threadIdx.x >> 4; r < nr; r += TILE_THREADS / 16) {
+        const int4 v = *reinterpret_cast<const int4*>(sbox + r * BOX_PITCH + 4 * q);
+        // two adjacent cells per 64-bit atomic: lo + 2^32 hi is exact in
+        // int64 and decodes uniquely while each cell's total fits int32
+        unsigned long long* R = reinterpret_cast<unsigned long long*>(rows[r] + c);
+        if (v.x | v.y)
+          atomicAdd(R, (unsigned long long)((long long)v.x + ((long long)v.y << 32)));
+        if (v.z | v.w)
+          atomicAdd(R + 1, (unsigned long long)((long long)v.z + ((long long)v.w << 32)));
+      }
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int c0 = wrap_once(b.lo[2] + lane, g.n3);
+  int c1 = wrap_once(b.lo[2] + lane + 32, g.n3);
+  for (int u1 = 0; u1 < b.ext[0]; ++u1) {
+    int p1 = b.lo[0] + u1;
+    if constexpr (!DIST) p1 = wrap_once(p1, g.n1);
+    int* P = reinterpret_cast<int*>(dst.plane_ptr(p1, g));
+    const int* SP = sbox + u1 * b.ext[1] * BOX_PITCH;
+    for (int u2 = warp; u2 < b.ext[1]; u2 += TILE_THREADS / 32) {
+      int* R = P + size_t(wrap_once(b.lo[1] + u2, g.n2)) * g.n3;
+      const int* S = SP + u2 * BOX_PITCH;
+      if (lane < b.ext[2] && S[lane]) fixed_add(R + c0, S[lane], fixed_packed(g));
+      if (lane + 32 < b.ext[2] && S[lane + 32]) fixed_add(R + c1, S[lane + 32], fixed_packed(g));
+    }
+  }
+}
+
 // ---- per-point stencil in box coordinates ---------------------------------
 
 template <int DEG>
@@ -380,6 +422,15 @@ __device__ __noinline__ float point_gather(const Geo& g, const SrcField<DIST> sr
   Stencil<DEG> st;
   st.template build<DIST>(g, i, j, k, d1, d2, d3);
   return st.gather(g, src);
+}
+
+template <int DEG, bool DIST>
+__device__ __noinline__ void point_scatter_fixed(const Geo& g, const DstField<DIST> dst, int i,
+                                                 int j, int k, float d1, float d2, float d3,
+                                                 float zS) {
+  Stencil<DEG> st;
+  st.template build<DIST>(g, i, j, k, d1, d2, d3);
+  st.scatter_fixed(g, dst, zS);
 }
 
 template <int DEG, bool DIST>

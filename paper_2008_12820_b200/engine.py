@@ -104,6 +104,11 @@ class Context:
     def synchronize(self):
         check(lib().vreg_ctx_synchronize(self.h))
 
+    def set_deterministic(self, on=True):
+        """Exact fixed-point transpose sweeps (bitwise reproducible and
+        independent of the GPU count); default fp32 L2 reductions."""
+        check(lib().vreg_ctx_set_deterministic(self.h, int(on)))
+
     def enable_timers(self, on=True):
         check(lib().vreg_ctx_enable_timers(self.h, int(on)))
 

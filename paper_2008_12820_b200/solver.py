@@ -93,6 +93,8 @@ _SOLVER_SIGS = {
     "vreg_solver_matvec_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "vreg_solver_matvec_host_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "vreg_solver_wait": (C.c_int, [C.c_void_p]),
+    "vreg_solver_report_text": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, C.c_size_t,
+                                          C.POINTER(C.c_size_t)]),
     "vreg_solver_precond": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_double, C.c_void_p,
                                       C.POINTER(C.c_uint64)]),
     "vreg_solver_register": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_double),
@@ -194,6 +196,17 @@ class Solver:
         cnt = (C.c_uint64 * 21)()
         check(lib().vreg_solver_register(self.h, _p(v), rep, cnt))
         return v, dict(zip(REPORT_NAMES, list(rep))), dict(zip(COUNTER_NAMES, list(cnt)))
+
+    def report_text(self, which="report"):
+        """Rendered report of the last register(): "report" (deterministic,
+        no timings), "timings" or "residuals" (CSV of PCG relative residuals)
+        -- include/vreg_b200/report.hpp."""
+        k = {"report": 0, "timings": 1, "residuals": 2}[which]
+        n = C.c_size_t()
+        check(lib().vreg_solver_report_text(self.h, k, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        check(lib().vreg_solver_report_text(self.h, k, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
 
     def counters(self):
         cnt = (C.c_uint64 * 21)()

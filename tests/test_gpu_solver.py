@@ -159,3 +159,31 @@ def test_fixed_registration_counters_match_reference(ctx):
                   "pc_h0_apply", "pc_refresh"):
             assert cnt[k] == rcnt[k], (pc, k, cnt[k], rcnt[k])
         assert abs(rep["final_mismatch"] / rrep["final_mismatch"] - 1) < 1e-3
+
+
+def test_report_rendering_is_deterministic(ctx):
+    """render_report (reference report.hpp:79-84 declares it; SPEC.md:578:
+    reruns give a bit-identical report) and the residual CSV, 32^3 fixed run
+    with continuation (two levels, InvA -> 2LInvH0 switch)."""
+    n = 32
+    texts = []
+    ctx.set_deterministic(True)  # exact fixed-point transpose sweeps
+    for _ in range(2):
+        cfg = Config(fixed_gn=1, fixed_pcg=3)
+        s = Solver(ctx, n, cfg)
+        s.syn_images()
+        _, rep, _ = s.register()
+        texts.append((s.report_text("report"), s.report_text("residuals"), s.report_text("timings")))
+        s.close()
+    ctx.set_deterministic(False)
+    (r1, c1, t1), (r2, c2, _) = texts
+    assert r1 == r2 and c1 == c2
+    lines = r1.splitlines()
+    assert lines[0] == "vreg_b200 report" and lines[1].startswith("grid 32 32 32 nt 4 p 1")
+    levels = [ln for ln in lines if ln.startswith("level ")]
+    assert len(levels) == int(rep["levels"]) and " pc inva switched 1 " in levels[0]
+    assert lines[-1].startswith("final mismatch") and f" gn {int(rep['total_gn'])} " in lines[-1]
+    rows = c1.strip().splitlines()
+    assert rows[0] == "level,beta,gn_iter,pcg_iter,rel_residual"
+    assert len(rows) - 1 == int(rep["total_pcg"]) + int(rep["total_gn"])  # + initial residuals
+    assert t1.startswith("phases_s total")

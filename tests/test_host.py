@@ -126,3 +126,34 @@ def test_halo_protocol_and_p_independent_fold_gloo(world):
     for rank, halos, fold_equal in res:
         assert all(halos.values()), (rank, halos)
         assert fold_equal
+
+
+def test_volume_file_roundtrip_and_errors(tmp_path):
+    """VolumeFile "VRG1": bitwise round trip for both
+    scalar kinds and component counts; bad magic / truncated payload rejected."""
+    from paper_2008_12820_b200 import VregError
+    from paper_2008_12820_b200.volume import load_volume, save_volume
+    rng = np.random.default_rng(7)
+    for dt, shape in ((np.float32, (6, 5, 4)), (np.float64, (3, 6, 5, 4)),
+                      (np.float32, (3, 2, 3, 4)), (np.float64, (4, 4, 4))):
+        a = rng.standard_normal(shape).astype(dt)
+        p = tmp_path / "v.vrg"
+        save_volume(p, a)
+        raw = p.read_bytes()
+        assert raw[:4] == b"VRG1" and len(raw) == 18 + a.nbytes
+        assert np.frombuffer(raw[4:16], "<u4").tolist() == list(shape[-3:])
+        assert raw[16] == (0 if dt == np.float32 else 1) and raw[17] == (3 if len(shape) == 4 else 1)
+        b = load_volume(p)
+        assert b.dtype == a.dtype and b.shape == a.shape and b.tobytes() == a.tobytes()
+    bad = tmp_path / "bad.vrg"
+    bad.write_bytes(b"VRG2" + raw[4:])
+    with pytest.raises(VregError) as e:
+        load_volume(bad)
+    assert e.value.kind == "io_error"
+    bad.write_bytes(raw[:-4])
+    with pytest.raises(VregError) as e:
+        load_volume(bad)
+    assert e.value.kind == "io_error"
+    with pytest.raises(VregError) as e:
+        load_volume(tmp_path / "missing.vrg")
+    assert e.value.kind == "io_error"

@@ -35,9 +35,13 @@ def run(ctx, dims, beta):
     grad = s.gradient()
     vt = (-grad).contiguous()
     H = s.matvec(vt)
+    ctx.set_deterministic(True)  # exact fixed-point transpose: bitwise p-independent
+    Hd = s.matvec(vt)
+    ctx.set_deterministic(False)
     P, _ = s.precond("inva", vt, 0.5)
     m0, m1 = s.images()
     out = {"J": J, "grad": ctx.to_global(g, grad), "H": ctx.to_global(g, H),
+           "Hdet": ctx.to_global(g, Hd),
            "P": ctx.to_global(g, P), "m1": ctx.to_global(g, m1)}
     s.close()
     cfg2 = Config(continuation=False, beta_target=beta, precond="inva", fixed_gn=2, fixed_pcg=3)
@@ -89,7 +93,8 @@ def main():
         ref = run(single, dims, beta)
         res["J_rel"] = abs(dist_out["J"]["total"] / ref["J"]["total"] - 1)
         res["mismatch_rel"] = abs(dist_out["J"]["mismatch"] / ref["J"]["mismatch"] - 1)
-        for k in ("m1", "grad", "H", "P", "v", "regop", "restrict", "high_pass", "P2", "v2l"):
+        for k in ("m1", "grad", "H", "Hdet", "P", "v", "regop", "restrict", "high_pass", "P2",
+                  "v2l"):
             res[f"{k}_rel"] = rel(dist_out[k], ref[k].astype(np.float64))
         res["solve_mismatch_rel"] = abs(dist_out["solve"]["final_mismatch"] /
                                         ref["solve"]["final_mismatch"] - 1)
@@ -99,7 +104,8 @@ def main():
               res["H_rel"] < 1e-5 and res["P_rel"] < 1e-5 and res["v_rel"] < 1e-4 and
               res["solve_mismatch_rel"] < 1e-4 and res["restrict_rel"] < 1e-5 and
               res["high_pass_rel"] < 1e-5 and res["P2_rel"] < 1e-4 and res["v2l_rel"] < 1e-4 and
-              res["solve2l_mismatch_rel"] < 1e-4 and res["regop_rel"] == 0.0)
+              res["solve2l_mismatch_rel"] < 1e-4 and res["regop_rel"] == 0.0 and
+              res["Hdet_rel"] == 0.0)
         res["ok"] = ok
         print(json.dumps(res), flush=True)
         single.close()
