@@ -139,6 +139,16 @@ def ncu_traffic():
         return None
 
 
+def ncu_smem_wavefronts():
+    """Per-launch shared-memory wavefronts (ncu l1tex__data_pipe_lsu_wavefronts_
+    mem_shared) of the SL kernels from profiles/smem_wavefronts.json, or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "smem_wavefronts.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 # --------------------------------------------------------------- CPU legs ----
 
 def cpu_reference_sample(n=128, matvecs=1):
@@ -378,6 +388,15 @@ def run_ours(args):
             if bpv:
                 ach = bpv * Nloc / per_launch_s / 1e9
                 roof.update({"achieved": ach, "frac": ach / peak})
+            # the SL sweeps are shared-memory-pipe bound (64 taps / point):
+            # wavefronts per launch vs one wavefront per SM clock
+            wf = ncu_smem_wavefronts().get(name)
+            sm_hz = (clk.summary().get("sm_mhz") or 0) * 1e6
+            if wf and sm_hz:
+                nsm = torch.cuda.get_device_properties(local).multi_processor_count
+                roof["smem_pipe"] = {"wavefronts_per_launch": wf,
+                                     "frac": wf / (per_launch_s * nsm * sm_hz),
+                                     "peak": "1 wavefront / SM / clock"}
         matvec_bytes = bytes_per_voxel(NT) * (Nvox // world)
         share = {k: round(v["seconds"] / (ms * 1e-3) , 4) for k, v in kstats.items()}
         fft_s = t_after["fft"] - t_before["fft"]

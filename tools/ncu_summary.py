@@ -33,6 +33,9 @@ METRICS = {
     "smsp__inst_executed.sum": "warp_inst",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_bank_conflicts",
     "sm__issue_active.avg.pct_of_peak_sustained_elapsed": "issue_active_pct",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "smem_wavefronts",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active": "lsu_pipe_pct",
+    "sm__cycles_elapsed.avg.per_second": "sm_hz",
 }
 STALLS = ["long_scoreboard", "barrier", "mio_throttle", "short_scoreboard", "wait", "selected",
           "not_selected", "math_pipe_throttle", "lg_throttle"]
@@ -108,6 +111,14 @@ def main():
             if re.search(pat, k["kernel"]) and "dram_read" in k:
                 traffic[timer] = k["dram_read"] + k.get("dram_write", 0.0)
     json.dump(traffic, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
+    # shared-memory wavefronts per launch (the SL kernels' binding pipe)
+    wpath = os.path.join(PROF, "smem_wavefronts.json")
+    wf = json.load(open(wpath)) if os.path.exists(wpath) else {}
+    for k in f:
+        for pat, timer in TIMER:
+            if re.search(pat, k["kernel"]) and "smem_wavefronts" in k:
+                wf[timer] = k["smem_wavefronts"]
+    json.dump(wf, open(wpath, "w"), indent=1)
     for k in f:
         print(k["kernel"][:60], {x: round(k[x], 1) for x in ("duration", "dram_read", "dram_write",
                                                            "dram_pct", "warps_active_pct",
