@@ -418,6 +418,37 @@ class CudaEngine {
   Field high_pass_field(const Field& f) const { return high_pass_impl<1>(f); }
   VField high_pass_field(const VField& v) const { return high_pass_impl<3>(v); }
 
+  // Fused fine-grid steps of the two-level preconditioner on one rank
+  // (precond.hpp:143-160): begin returns (restrict(r), restrict(InvA r)) from
+  // one forward transform, end returns prolong(s_c) + high_pass(InvA r) with
+  // one inverse. Logical counters as InvA + two restrictions / prolongation
+  // + high pass, so the cost model is unchanged.
+  bool two_level_fused() const {
+    const char* e = std::getenv("VREG_TWO_LEVEL_UNFUSED");
+    return workers() == 1 && !coarse_ && !(e && e[0] == '1');
+  }
+  std::pair<VField, VField> two_level_begin(const VField& r, Real beta_pc) const {
+    if (beta_pc <= Real(0)) throw parameter_error("regularization beta must be > 0");
+    count_fft(3, 3);
+    auto& c = state_->counters;
+    c.fft_forward += 6;
+    c.fft_inverse_coarse += 6;
+    VField rc(state_->dev, grid_.coarse()), sc(state_->dev, grid_.coarse());
+    const vreg_grid g = vg();
+    check(vreg_two_level_begin(ctx(), &g, r.data(), beta_pc, rc.data(), sc.data()));
+    return {std::move(rc), std::move(sc)};
+  }
+  VField two_level_end(const VField& s_c) const {
+    auto& c = state_->counters;
+    c.fft_forward_coarse += 3;
+    c.fft_inverse += 3;
+    count_fft(3, 3);
+    VField out = make_vfield();
+    const vreg_grid g = vg();
+    check(vreg_two_level_end(ctx(), &g, s_c.data(), out.data()));
+    return out;
+  }
+
   // ---- semi-Lagrangian support (engine.hpp:108-169) ----
   Char make_characteristics(const VField& v, int degree) const {
     state_->counters.characteristics++;

@@ -416,13 +416,21 @@ class Preconditioner {
       return s;
     }
     CudaEngine& ce = *coarse_;
+    auto inner = [&](const DVField& r_c, DVField& s_c) {
+      auto res = pcg(
+          ce, [&](const DVField& x) { return h0_matvec(ce, x, *grad_mref_coarse_, beta_pc_); },
+          [&](const DVField& x) { return ce.inv_regop(x, beta_pc_); }, r_c, s_c, opt);
+      account(res, stats);
+    };
+    if (eng_->two_level_fused()) {  // one fine forward + one fine inverse transform
+      auto rs = eng_->two_level_begin(r, beta_pc_);
+      inner(rs.first, rs.second);
+      return eng_->two_level_end(rs.second);
+    }
     DVField s_f = eng_->inv_regop(r, beta_pc_);
     DVField r_c = eng_->restrict_to_coarse(r);
     DVField s_c = eng_->restrict_to_coarse(s_f);
-    auto res = pcg(
-        ce, [&](const DVField& x) { return h0_matvec(ce, x, *grad_mref_coarse_, beta_pc_); },
-        [&](const DVField& x) { return ce.inv_regop(x, beta_pc_); }, r_c, s_c, opt);
-    account(res, stats);
+    inner(r_c, s_c);
     DVField out = eng_->prolong_to_fine(s_c);
     DVField hp = eng_->high_pass_field(s_f);
     axpy(Real(1), hp, out);

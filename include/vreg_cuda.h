@@ -182,6 +182,15 @@ int vreg_prolong(vreg_ctx, const vreg_grid* fine, int ncomp, const float* fc, fl
 int vreg_high_pass(vreg_ctx, const vreg_grid*, int ncomp, const float* f, float* out);
 /* H0 s = beta_pc A s (unit zero mode) + grad_mref (grad_mref . s)
  * (precond.hpp:30-42). */
+/* Fused fine-grid steps of the two-level preconditioner (precond.hpp:143-160)
+ * on one rank: begin writes rc3 = restrict(r3) and sc3 = restrict(InvA r3) on
+ * the coarse grid (n/2) from ONE forward transform of r3 and keeps InvA r3's
+ * spectrum; end writes out3 = prolong(sc3) + high_pass(InvA r3) with one
+ * inverse transform. VREG_ECONFIG on several ranks. */
+int vreg_two_level_begin(vreg_ctx ctx, const vreg_grid* g, const float* r3, double beta_pc,
+                         float* rc3, float* sc3);
+int vreg_two_level_end(vreg_ctx ctx, const vreg_grid* g, const float* sc3, float* out3);
+
 int vreg_h0_matvec(vreg_ctx, const vreg_grid*, const float* s3, const float* grad_mref3,
                    double beta_pc, float* out3);
 /* Half-space spectrum of a scalar field, interleaved complex64,

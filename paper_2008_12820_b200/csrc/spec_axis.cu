@@ -117,7 +117,9 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 2) k_axis_d2(int n1
                                                          const float* __restrict__ v,
                                                          float* __restrict__ out,
                                                          const float2* __restrict__ tw,
-                                                         float coef, int accumulate) {
+                                                         float coef, int accumulate,
+                                                         const double* __restrict__ bias_sums,
+                                                         double bias_scale) {
   constexpr int T1 = AxisShape<N>::T1, NP = AxisShape<N>::NP, WQ = 2 * NP;
   constexpr int R2 = N / T1;
   constexpr int SK = T1 + 1, SP = R2 * SK + 1;  // odd float2 pitches: conflict-free
@@ -127,6 +129,8 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 2) k_axis_d2(int n1
   const int comp = t / tiles, tile = t - comp * tiles;
   const float* vc = v + size_t(comp) * nloc;
   float* oc = out + size_t(comp) * nloc;
+  // unit null-mode symbol: + beta * mean(v_c) on the writing (first) pass
+  const float bias = bias_sums ? float(bias_scale * bias_sums[comp]) : 0.0f;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   (void)w;
   (void)l;
@@ -205,8 +209,8 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 2) k_axis_d2(int n1
         q[0] += a[m].x;
         q[qs] += a[m].y;
       } else {
-        q[0] = a[m].x;
-        q[qs] = a[m].y;
+        q[0] = a[m].x + bias;
+        q[qs] = a[m].y + bias;
       }
     } else {
       float2* q2 = reinterpret_cast<float2*>(q);
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 2) k_axis_d2(int n1
         const float2 o = *q2;
         *q2 = make_float2(o.x + a[m].x, o.y + a[m].y);
       } else {
-        *q2 = a[m];
+        *q2 = make_float2(a[m].x + bias, a[m].y + bias);
       }
     }
   }
@@ -247,7 +251,8 @@ struct AxisGeom {
 
 template <int AX>
 void launch_axis(vreg_ctx ctx, const AxisGeom& s, int n, const float* v3, float* out3,
-                 double beta, int accumulate, int ctas_per_sm) {
+                 double beta, int accumulate, int ctas_per_sm,
+                 const double* bias_sums = nullptr, double bias_scale = 0.0) {
   const int wq = n <= 512 ? 32 : 16;  // 2 * AxisShape<n>::NP
   const int tiles = AX == 3 ? int(size_t(s.n1l) * s.n2 / wq)
                             : (AX == 2 ? s.n1l : s.n2) * (s.n3 / wq);
@@ -273,7 +278,8 @@ void launch_axis(vreg_ctx ctx, const AxisGeom& s, int n, const float* v3, float*
     }();                                                                                   \
     (void)attr;                                                                            \
     k_axis_d2<NN, AX><<<grid, AX_THREADS, smem, ctx->stream>>>(s.n1l, s.n2, s.n3, tiles, v3, \
-                                                               out3, tw, coef, accumulate); \
+                                                               out3, tw, coef, accumulate, \
+                                                               bias_sums, bias_scale);     \
     break;                                                                                 \
   }
   switch (n) {
@@ -461,12 +467,40 @@ void dist_axis1(vreg_ctx ctx, const Slab& s, const float* v3, float* out3, doubl
   check_launch();
 }
 
+// Per-component sums of v (the k = 0 mode), deterministic: fixed block
+// partials, then one ordered fold per component.
+constexpr int SUM_BLOCKS = 296;
+__global__ void k_comp_partials(size_t n, const float* __restrict__ v, double* __restrict__ part) {
+  const int c = blockIdx.y;
+  const float* vc = v + size_t(c) * n;
+  double acc = 0.0;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    acc += double(vc[i]);
+  __shared__ double sh[256];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (int(threadIdx.x) < st) sh[threadIdx.x] += sh[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[c * SUM_BLOCKS + blockIdx.x] = sh[0];
+}
+__global__ void k_comp_fold(const double* __restrict__ part, double* __restrict__ sums) {
+  const int c = threadIdx.x >> 5, l = threadIdx.x & 31;  // warp c folds component c
+  double acc = 0.0;
+  for (int b = l; b < SUM_BLOCKS; b += 32) acc += part[c * SUM_BLOCKS + b];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if (l == 0) sums[c] = acc;
+}
+
 }  // namespace
 
 // out3 = beta (-Lap) v3 via three 1-D spectral passes; false if the grid is
 // outside the fast path (non power-of-two or > 512 sizes, x2 not divisible
 // by the rank count).
-bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, float* out3) {
+bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, float* out3,
+                     bool unit_zero) {
   if (!axis_size_ok(s.n1) || !axis_size_ok(s.n2) || !axis_size_ok(s.n3)) return false;
   if (ctx->nranks > 1 && s.n2 % ctx->nranks != 0) return false;
   static const bool off = [] {
@@ -480,7 +514,20 @@ bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, 
     return e ? std::atoi(e) : 0;
   }();
   const AxisGeom loc{s.n1l, s.n2, s.n3};
-  launch_axis<3>(ctx, loc, s.n3, v3, out3, beta, 0, cap);
+  const double* sums = nullptr;
+  if (unit_zero) {  // symbol beta at k = 0: + beta * mean(v_c) (spectral.cpp:48-70)
+    double* part = static_cast<double*>(workspace(ctx, "axis_part", 3 * SUM_BLOCKS * sizeof(double)));
+    double* sm = static_cast<double*>(workspace(ctx, "axis_sums", 4 * sizeof(double)));
+    k_comp_partials<<<dim3(SUM_BLOCKS, 3), 256, 0, ctx->stream>>>(s.local(), v3, part);
+    k_comp_fold<<<1, 96, 0, ctx->stream>>>(part, sm);
+    count_launch(ctx, 2);
+    check_launch();
+    if (ctx->nranks > 1)
+      VB_NCCL(ncclAllReduce(sm, sm, 3, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    sums = sm;
+  }
+  launch_axis<3>(ctx, loc, s.n3, v3, out3, beta, 0, cap, sums,
+                 beta / double(s.global()));
   launch_axis<2>(ctx, loc, s.n2, v3, out3, beta, 1, cap);
   if (ctx->nranks == 1)
     launch_axis<1>(ctx, loc, s.n1, v3, out3, beta, 1, cap);

@@ -164,6 +164,22 @@ __global__ void k_restrict(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3,
 
 // Fine half spectrum from the coarse one: coarse modes split evenly over
 // their fine partners, zero outside the band (spectral.cpp:176-203).
+__device__ __forceinline__ float2 prolong_elem(int nf1, int nf2, int nc1, int nc2, int nc3,
+                                               const float2* __restrict__ Fc, int f1, int f2,
+                                               int f3, float scale) {
+  const int hc = nc3 / 2 + 1;
+  const int nu1 = f1 <= nf1 / 2 ? f1 : f1 - nf1;
+  const int nu2 = f2 <= nf2 / 2 ? f2 : f2 - nf2;
+  if (abs(nu1) <= nc1 / 2 && abs(nu2) <= nc2 / 2 && f3 <= nc3 / 2) {
+    const int cnt = (abs(nu1) == nc1 / 2 ? 2 : 1) * (abs(nu2) == nc2 / 2 ? 2 : 1) *
+                    (f3 == nc3 / 2 ? 2 : 1);
+    const float2 v = Fc[(size_t(pmod(nu1, nc1)) * nc2 + pmod(nu2, nc2)) * hc + f3];
+    const float m = scale / float(cnt);
+    return make_float2(v.x * m, v.y * m);
+  }
+  return make_float2(0.f, 0.f);
+}
+
 __global__ void k_prolong(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3, int ncomp,
                           const float2* __restrict__ Fc, float2* __restrict__ Ff, float scale) {
   const int hc = nc3 / 2 + 1, hf = nf3 / 2 + 1;
@@ -174,61 +190,72 @@ __global__ void k_prolong(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3, 
     const int c = int(e / ncf);
     const size_t r = e % ncf;
     const int f3 = int(r % hf), f2 = int((r / hf) % nf2), f1 = int(r / (size_t(hf) * nf2));
-    const int nu1 = f1 <= nf1 / 2 ? f1 : f1 - nf1;
-    const int nu2 = f2 <= nf2 / 2 ? f2 : f2 - nf2;
-    float2 out = make_float2(0.f, 0.f);
-    if (abs(nu1) <= nc1 / 2 && abs(nu2) <= nc2 / 2 && f3 <= nc3 / 2) {
-      const int cnt = (abs(nu1) == nc1 / 2 ? 2 : 1) * (abs(nu2) == nc2 / 2 ? 2 : 1) *
-                      (f3 == nc3 / 2 ? 2 : 1);
-      const float2 v = Fc[size_t(c) * ncc + (size_t(pmod(nu1, nc1)) * nc2 + pmod(nu2, nc2)) * hc + f3];
-      const float m = scale / float(cnt);
-      out = make_float2(v.x * m, v.y * m);
-    }
-    Ff[e] = out;
+    Ff[e] = prolong_elem(nf1, nf2, nc1, nc2, nc3, Fc + size_t(c) * ncc, f1, f2, f3, scale);
   }
 }
 
 // High pass with the alias-pair remainder on the coarse Nyquist lines
 // (spectral.cpp:205-240); out of place (reads the original spectrum).
+__device__ __forceinline__ float2 high_pass_elem(int n1, int n2, int n3,
+                                                 const float2* __restrict__ F, int k1, int k2,
+                                                 int k3, float scale) {
+  const int h = n3 / 2 + 1;
+  const int b1 = n1 / 4, b2 = n2 / 4, b3 = n3 / 4;
+  const int nu1 = k1 <= n1 / 2 ? k1 : k1 - n1;
+  const int nu2 = k2 <= n2 / 2 ? k2 : k2 - n2;
+  float2 v = F[(size_t(k1) * n2 + k2) * h + k3];
+  if (!(abs(nu1) > b1 || abs(nu2) > b2 || k3 > b3)) {
+    const bool y1 = abs(nu1) == b1, y2 = abs(nu2) == b2, y3 = k3 == b3;
+    if (!y1 && !y2 && !y3) {
+      v = make_float2(0.f, 0.f);
+    } else {
+      float ax = 0.f, ay = 0.f;
+      int cnt = 0;
+      for (int s1 = 0; s1 < (y1 ? 2 : 1); ++s1)
+        for (int s2 = 0; s2 < (y2 ? 2 : 1); ++s2)
+          for (int s3 = 0; s3 < (y3 ? 2 : 1); ++s3) {
+            const int m1 = y1 ? (s1 ? n1 - b1 : b1) : k1;
+            const int m2 = y2 ? (s2 ? n2 - b2 : b2) : k2;
+            const int m3 = y3 ? (s3 ? n3 - b3 : b3) : k3;
+            const float2 w = full_at(F, n1, n2, n3, m1, m2, m3);
+            ax += w.x;
+            ay += w.y;
+            ++cnt;
+          }
+      v.x -= ax / float(cnt);
+      v.y -= ay / float(cnt);
+    }
+  }
+  return make_float2(v.x * scale, v.y * scale);
+}
+
 __global__ void k_high_pass(int n1, int n2, int n3, int ncomp, const float2* __restrict__ Fin,
                             float2* __restrict__ Fout, float scale) {
   const int h = n3 / 2 + 1;
   const size_t nc = size_t(n1) * n2 * h;
   const size_t total = nc * size_t(ncomp);
-  const int b1 = n1 / 4, b2 = n2 / 4, b3 = n3 / 4;
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
     const int c = int(e / nc);
     const size_t r = e % nc;
     const int k3 = int(r % h), k2 = int((r / h) % n2), k1 = int(r / (size_t(h) * n2));
-    const int nu1 = k1 <= n1 / 2 ? k1 : k1 - n1;
-    const int nu2 = k2 <= n2 / 2 ? k2 : k2 - n2;
-    const float2* F = Fin + size_t(c) * nc;
-    float2 v = F[r];
-    if (!(abs(nu1) > b1 || abs(nu2) > b2 || k3 > b3)) {
-      const bool y1 = abs(nu1) == b1, y2 = abs(nu2) == b2, y3 = k3 == b3;
-      if (!y1 && !y2 && !y3) {
-        v = make_float2(0.f, 0.f);
-      } else {
-        float ax = 0.f, ay = 0.f;
-        int cnt = 0;
-        for (int s1 = 0; s1 < (y1 ? 2 : 1); ++s1)
-          for (int s2 = 0; s2 < (y2 ? 2 : 1); ++s2)
-            for (int s3 = 0; s3 < (y3 ? 2 : 1); ++s3) {
-              const int m1 = y1 ? (s1 ? n1 - b1 : b1) : k1;
-              const int m2 = y2 ? (s2 ? n2 - b2 : b2) : k2;
-              const int m3 = y3 ? (s3 ? n3 - b3 : b3) : k3;
-              const float2 w = full_at(F, n1, n2, n3, m1, m2, m3);
-              ax += w.x;
-              ay += w.y;
-              ++cnt;
-            }
-        v.x -= ax / float(cnt);
-        v.y -= ay / float(cnt);
-      }
-    }
-    Fout[e] = make_float2(v.x * scale, v.y * scale);
+    Fout[e] = high_pass_elem(n1, n2, n3, Fin + size_t(c) * nc, k1, k2, k3, scale);
   }
+}
+
+// Fused end of the two-level apply: G = prolong(Fc) + high_pass(Ff) on the
+// fine half spectrum (3-D grid: k3 over x, k2 over y, (comp, k1) over z).
+__global__ void k_prolong_plus_hp(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3,
+                                  const float2* __restrict__ Fc, const float2* __restrict__ Ff,
+                                  float2* __restrict__ G, float scale_p, float scale_h) {
+  const int hf = nf3 / 2 + 1, hc = nc3 / 2 + 1;
+  const int k3 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k3 >= hf) return;
+  const int k2 = blockIdx.y, c = blockIdx.z / nf1, k1 = blockIdx.z - c * nf1;
+  const size_t ncf = size_t(nf1) * nf2 * hf, ncc = size_t(nc1) * nc2 * hc;
+  const float2 a = prolong_elem(nf1, nf2, nc1, nc2, nc3, Fc + c * ncc, k1, k2, k3, scale_p);
+  const float2 b = high_pass_elem(nf1, nf2, nf3, Ff + c * ncf, k1, k2, k3, scale_h);
+  G[c * ncf + (size_t(k1) * nf2 + k2) * hf + k3] = make_float2(a.x + b.x, a.y + b.y);
 }
 
 // out_c += g_c (g . s) (precond.hpp:36-37)
@@ -300,15 +327,17 @@ void apply_symbol(vreg_ctx ctx, const SpecDesc& d, int ncomp, float2* F, double 
   check_launch();
 }
 
-bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, float* out3);
+bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, float* out3,
+                     bool unit_zero);
 
 // out3 = beta A v3 (or its inverse); used by the fused matvec too. The
-// forward operator with a zero null-mode symbol is separable and runs as
-// three 1-D spectral passes (spec_axis.cu) where the grid allows.
+// forward operator is separable (|k|^2 = k1^2 + k2^2 + k3^2; a unit null-mode
+// symbol is + beta mean(v)) and runs as three 1-D spectral passes
+// (spec_axis.cu) where the grid allows; the inverse stays on cuFFT.
 void spectral_regop(vreg_ctx ctx, const Slab& s, const float* v3, double beta, bool unit_zero,
                     bool inverse, float* out3) {
   require(beta > 0.0, VREG_EPARAM, "regularization beta must be > 0");
-  if (!inverse && !unit_zero && regop_separable(ctx, s, v3, beta, out3)) return;
+  if (!inverse && regop_separable(ctx, s, v3, beta, out3, unit_zero)) return;
   const SpecDesc d = spec_desc(ctx, s);
   float2* F = spec_buffer(ctx, d, 3, "spec3");
   fft_forward(ctx, s, 3, v3, F);
@@ -467,6 +496,60 @@ int vreg_fft_forward(vreg_ctx ctx, const vreg_grid* g, const float* f, float* ou
     Slab s = slab_of(ctx, g);
     require(ctx->nranks == 1, VREG_ECONFIG, "fft_forward test hook is single-rank");
     fft_forward(ctx, s, 1, f, reinterpret_cast<float2*>(out_c));
+  });
+}
+
+// Fused fine-grid work of the two-level preconditioner (precond.hpp:143-160)
+// on one rank: one forward transform of r and one inverse for the result.
+//   begin: F = R2C(r); rc = C2R_c(restrict(F)); F *= 1/(beta |k|^2) (the
+//          spectrum of InvA r, zero mode 1/beta); sc = C2R_c(restrict(F));
+//          F is kept for the end.
+//   end:   out = C2R(prolong(R2C_c(sc)) + high_pass(F)).
+int vreg_two_level_begin(vreg_ctx ctx, const vreg_grid* g, const float* r3, double beta_pc,
+                         float* rc3, float* sc3) {
+  return guard([&] {
+    require(ctx->nranks == 1, VREG_ECONFIG, "fused two-level apply is single-rank");
+    require(beta_pc > 0.0, VREG_EPARAM, "regularization beta must be > 0");
+    Slab s = slab_of(ctx, g);
+    vreg_grid gc{s.n1 / 2, s.n2 / 2, s.n3 / 2, s.nt};
+    Slab sc = slab_of(ctx, &gc);
+    const SpecDesc df = spec_desc(ctx, s), dc = spec_desc(ctx, sc);
+    float2* F = spec_buffer(ctx, df, 3, "tl_F");
+    float2* Fc = spec_buffer(ctx, dc, 3, "tl_Fc");
+    fft_forward(ctx, s, 3, r3, F);
+    const float rs = float(1.0 / double(s.global()));
+    k_restrict<<<blocks_for(dc.nc * 3, kT), kT, 0, ctx->stream>>>(s.n1, s.n2, s.n3, sc.n1, sc.n2,
+                                                                 sc.n3, 3, F, Fc, rs);
+    count_launch(ctx);
+    check_launch();
+    fft_inverse(ctx, sc, 3, Fc, rc3);
+    apply_symbol(ctx, df, 3, F, beta_pc, true, true, 1.0);
+    k_restrict<<<blocks_for(dc.nc * 3, kT), kT, 0, ctx->stream>>>(s.n1, s.n2, s.n3, sc.n1, sc.n2,
+                                                                 sc.n3, 3, F, Fc, rs);
+    count_launch(ctx);
+    check_launch();
+    fft_inverse(ctx, sc, 3, Fc, sc3);
+  });
+}
+
+int vreg_two_level_end(vreg_ctx ctx, const vreg_grid* g, const float* sc3, float* out3) {
+  return guard([&] {
+    require(ctx->nranks == 1, VREG_ECONFIG, "fused two-level apply is single-rank");
+    Slab s = slab_of(ctx, g);
+    vreg_grid gc{s.n1 / 2, s.n2 / 2, s.n3 / 2, s.nt};
+    Slab sc = slab_of(ctx, &gc);
+    const SpecDesc df = spec_desc(ctx, s), dc = spec_desc(ctx, sc);
+    float2* F = spec_buffer(ctx, df, 3, "tl_F");
+    float2* Fc = spec_buffer(ctx, dc, 3, "tl_Fc");
+    float2* G = spec_buffer(ctx, df, 3, "tl_G");
+    fft_forward(ctx, sc, 3, sc3, Fc);
+    const dim3 grid(unsigned((df.h + 127) / 128), unsigned(s.n2), unsigned(3 * s.n1));
+    k_prolong_plus_hp<<<grid, 128, 0, ctx->stream>>>(
+        s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, Fc, F, G, float(1.0 / double(sc.global())),
+        float(1.0 / double(s.global())));
+    count_launch(ctx);
+    check_launch();
+    fft_inverse(ctx, s, 3, G, out3);
   });
 }
 

@@ -120,12 +120,13 @@ def test_fd_nonsquare_and_constant(ctx):
 
 @pytest.mark.parametrize("shape", [(32, 32, 32), (64, 32, 128), (32, 256, 64), (512, 32, 32), (1024, 32, 32), (32, 32, 1024)])
 def test_regop_separable_passes(ctx, shape):
-    """Zero-null-mode regop runs as three 1-D spectral passes (spec_axis.cu)
-    on power-of-two grids; white noise exercises every mode incl. Nyquist.
-    unit_zero=True keeps the 3-D cuFFT route on the same grid."""
+    """The regop runs as three 1-D spectral passes (spec_axis.cu) on
+    power-of-two grids; white noise exercises every mode incl. Nyquist, the
+    per-component offsets the unit null-mode symbol (+ beta mean(v))."""
     g = ctx.grid(*shape)
     rng = np.random.default_rng(sum(shape))
     r = np.stack([random_smooth(shape, s) for s in (31, 32, 33)]) + 0.2 * rng.standard_normal((3, *shape))
+    r += np.array([0.7, -0.3, 0.0])[:, None, None, None]
     rd = dev(r)
     assert rel(host(ctx.regop(g, rd, 0.37, False)), ref.regop(r, 0.37, False)) < TOL
     assert rel(host(ctx.regop(g, rd, 0.37, True)), ref.regop(r, 0.37, True)) < TOL
