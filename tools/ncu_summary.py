@@ -42,7 +42,7 @@ STALLS = ["long_scoreboard", "barrier", "mio_throttle", "short_scoreboard", "wai
 
 # kernel name fragment -> bench.py timer name
 # kernel-name pattern -> bench.py timer name (demangled with or without casts)
-TIMER = [(r"k_scatter_tile<(\(int\))?3", "sl_scatter_sweep"),
+TIMER = [(r"k_scatter_tile(_fp)?<(\(int\))?3", "sl_scatter_sweep"),
          (r"k_gather_tile<(\(int\))?3, (\(bool\))?(0|false), (\(int\))?2>", "sl_inc_step"),
          (r"k_inc_u", "sl_inc_init"), (r"k_assemble", "sl_assemble"),
          (r"k_axis_d2<(\(int\))?\d+, (\(int\))?1>", "spec_axis1"),
