@@ -6,9 +6,8 @@
 // round-off). Weights come from the same Fornberg
 // recursion (fd.cpp:7-48), evaluated in fp64 and rounded once.
 //
-// Tiling: a CTA owns a 32 (x3) x 8 (x2) tile of one x1 plane and stages the
-// tile plus its x2/x3 halo of 4 in shared memory; x1 neighbours stream from
-// L2 (each plane is re-read by the 8 CTAs that need it, so HBM sees ~1x).
+// Tiling: see the x1-marching kernels below (register window along x1,
+// double-buffered shared tile with the x2/x3 halo of 4).
 #include <cmath>
 #include <vector>
 
@@ -86,84 +85,132 @@ __device__ __forceinline__ const float* fd_plane(const float* f, const float* lo
   }
 }
 
-// Stage tile (TY+2H) x (TX+2H) of plane P into smem with x2/x3 wrap.
-__device__ __forceinline__ void stage_tile(float (*t)[TX + 2 * H], const float* P, int j0, int k0,
-                                           const FdGeo& g) {
-  for (int y = threadIdx.y; y < TY + 2 * H; y += TY) {
-    int jj = (j0 + y - H) % g.n2;
-    jj = jj < 0 ? jj + g.n2 : jj;
-    const float* R = P + size_t(jj) * g.n3;
-    for (int x = threadIdx.x; x < TX + 2 * H; x += TX) {
-      int kk = (k0 + x - H) % g.n3;
-      kk = kk < 0 ? kk + g.n3 : kk;
-      t[y][x] = __ldg(R + kk);
+// ---- x1-marching kernels ----------------------------------------------------
+// A CTA owns a 32 (x3) x 8 (x2) column of the slab and marches FD_CH planes
+// along x1: each thread keeps its column's 9-plane window in registers (the
+// x1 stencil; the plane two steps ahead is already in flight), and the
+// current plane's tile + x2/x3 halo sits in a 3-deep ring of shared tiles
+// filled by 16-byte cp.async two planes ahead, so the loop never waits on a
+// fresh global load. Each input element is read from HBM about once; no
+// integer division is left in the loop. Same paired sums in the same order as
+// the per-plane formulation: bitwise identical results.
+#ifndef VB_FD_CH
+#define VB_FD_CH 16
+#endif
+constexpr int FD_CH = VB_FD_CH;  // planes per CTA
+constexpr int FD_RING = 3;  // shared tiles in flight
+constexpr int TW = TX + 2 * H;
+
+__device__ __forceinline__ int wrap_fd(int x, int n) { return x < 0 ? x + n : (x >= n ? x - n : x); }
+
+__device__ __forceinline__ void fd_cp16(float* smem, const float* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void fd_cp4(float* smem, const float* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void fd_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void fd_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Issue the tile + halo of plane P (rows j0-H .. j0+TY+H-1, columns k0-H ..
+// k0+TX+H-1, periodic) into t: 16-byte chunks when n3 % 4 == 0.
+__device__ __forceinline__ void stage_async(float (*t)[TW], const float* P, int j0, int k0,
+                                            const FdGeo& g) {
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  if ((g.n3 & 3) == 0) {
+    constexpr int CH = TW / 4;  // 10 chunks per row
+    for (int c = tid; c < (TY + 2 * H) * CH; c += TX * TY) {
+      const int y = c / CH, x4 = c - y * CH;
+      const float* R = P + size_t(wrap_fd(j0 + y - H, g.n2)) * g.n3;
+      fd_cp16(&t[y][4 * x4], R + wrap_fd(k0 - H + 4 * x4, g.n3));
+    }
+  } else {
+    for (int c = tid; c < (TY + 2 * H) * TW; c += TX * TY) {
+      const int y = c / TW, x = c - y * TW;
+      const float* R = P + size_t(wrap_fd(j0 + y - H, g.n2)) * g.n3;
+      fd_cp4(&t[y][x], R + wrap_fd(k0 - H + x, g.n3));
     }
   }
 }
 
-template <bool DIST>
-__global__ void __launch_bounds__(TX* TY) k_fd_grad(FdGeo g, const float* __restrict__ f,
-                                                    const float* __restrict__ lo,
-                                                    const float* __restrict__ hi, FdW w,
-                                                    float h1, float h2, float h3,
-                                                    float* __restrict__ out) {
-  __shared__ float t[TY + 2 * H][TX + 2 * H];
-  const int k0 = blockIdx.x * TX, j0 = blockIdx.y * TY, i = blockIdx.z;
-  stage_tile(t, fd_plane<DIST>(f, lo, hi, i, g), j0, k0, g);
-  __syncthreads();
-  const int k = k0 + threadIdx.x, j = j0 + threadIdx.y;
-  if (k >= g.n3 || j >= g.n2) return;
-  const int x = threadIdx.x + H, y = threadIdx.y + H;
-  float a3 = 0.f, a2 = 0.f, a1 = 0.f;
-#pragma unroll
-  for (int q = 1; q <= 4; ++q) {
-    a3 += w.c[q - 1] * (t[y][x + q] - t[y][x - q]);
-    a2 += w.c[q - 1] * (t[y + q][x] - t[y - q][x]);
-  }
-  const size_t off = size_t(j) * g.n3 + k;
-#pragma unroll
-  for (int q = 1; q <= 4; ++q)
-    a1 += w.c[q - 1] * (__ldg(fd_plane<DIST>(f, lo, hi, i + q, g) + off) -
-                        __ldg(fd_plane<DIST>(f, lo, hi, i - q, g) + off));
+template <bool DIST, bool DIV>
+__global__ void __launch_bounds__(TX* TY) k_fd_m(FdGeo g, const float* __restrict__ f,
+                                                 const float* __restrict__ lo,
+                                                 const float* __restrict__ hi, FdW w, float h1,
+                                                 float h2, float h3, float* __restrict__ out) {
+  // grad: f scalar; ring holds f. div: f = v (3 comps): the window follows v1,
+  // the rings hold v2 (x2 derivative) and v3 (x3 derivative).
+  constexpr int NR = DIV ? 2 : 1;
+  __shared__ __align__(16) float t[NR][FD_RING][TY + 2 * H][TW];
   const size_t N = size_t(g.n1l) * g.plane;
-  const size_t p = size_t(i) * g.plane + off;
-  out[p] = a1 * h1;
-  out[N + p] = a2 * h2;
-  out[2 * N + p] = a3 * h3;
-}
-
-template <bool DIST>
-__global__ void __launch_bounds__(TX* TY) k_fd_div(FdGeo g, const float* __restrict__ v,
-                                                   const float* __restrict__ lo,
-                                                   const float* __restrict__ hi, FdW w,
-                                                   float h1, float h2, float h3,
-                                                   float* __restrict__ out) {
-  __shared__ float t2[TY + 2 * H][TX + 2 * H];
-  __shared__ float t3[TY + 2 * H][TX + 2 * H];
-  const size_t N = size_t(g.n1l) * g.plane;
-  const int k0 = blockIdx.x * TX, j0 = blockIdx.y * TY, i = blockIdx.z;
-  stage_tile(t2, v + N + size_t(i) * g.plane, j0, k0, g);
-  stage_tile(t3, v + 2 * N + size_t(i) * g.plane, j0, k0, g);
-  __syncthreads();
+  const int k0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+  const int i0 = blockIdx.z * FD_CH, i1 = min(i0 + FD_CH, g.n1l);
   const int k = k0 + threadIdx.x, j = j0 + threadIdx.y;
-  if (k >= g.n3 || j >= g.n2) return;
-  const int x = threadIdx.x + H, y = threadIdx.y + H;
-  float a3 = 0.f, a2 = 0.f, a1 = 0.f;
+  const bool valid = k < g.n3 && j < g.n2;
+  const size_t off = valid ? size_t(j) * g.n3 + k : 0;
+  auto ring_src = [&](int r, int i) -> const float* {
+    if constexpr (DIV)
+      return f + size_t(r + 1) * N + size_t(i) * g.plane;
+    else
+      return fd_plane<DIST>(f, lo, hi, i, g);
+  };
+  // prologue: planes i0, i0+1 in flight
 #pragma unroll
-  for (int q = 1; q <= 4; ++q) {
-    a3 += w.c[q - 1] * (t3[y][x + q] - t3[y][x - q]);
-    a2 += w.c[q - 1] * (t2[y + q][x] - t2[y - q][x]);
+  for (int d = 0; d < 2; ++d) {
+    if (i0 + d < i1)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) stage_async(t[r][d], ring_src(r, i0 + d), j0, k0, g);
+    fd_commit();
   }
-  const size_t off = size_t(j) * g.n3 + k;
+  float win[2 * H + 1];
 #pragma unroll
-  for (int q = 1; q <= 4; ++q)
-    a1 += w.c[q - 1] * (__ldg(fd_plane<DIST>(v, lo, hi, i + q, g) + off) -
-                        __ldg(fd_plane<DIST>(v, lo, hi, i - q, g) + off));
-  // out = d1 v1; out += d2 v2; out += d3 v3 (fd.cpp:171-177)
-  float o = a1 * h1;
-  o += a2 * h2;
-  o += a3 * h3;
-  out[size_t(i) * g.plane + off] = o;
+  for (int q = 0; q <= 2 * H; ++q)
+    win[q] = valid ? __ldg(fd_plane<DIST>(f, lo, hi, i0 - H + q, g) + off) : 0.f;
+  float nxt = (valid && i0 + 1 < i1) ? __ldg(fd_plane<DIST>(f, lo, hi, i0 + H + 1, g) + off) : 0.f;
+  for (int i = i0; i < i1; ++i) {
+    const int b = (i - i0) % FD_RING;
+    fd_wait<1>();     // plane i landed (i+1 may still be in flight)
+    __syncthreads();  // ... for every thread; ring slot (i+2) % 3 is free
+    if (i + 2 < i1)
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        stage_async(t[r][(i + 2 - i0) % FD_RING], ring_src(r, i + 2), j0, k0, g);
+    fd_commit();
+    const float nxt2 =
+        (valid && i + 2 < i1) ? __ldg(fd_plane<DIST>(f, lo, hi, i + H + 2, g) + off) : 0.f;
+    if (valid) {
+      const int x = threadIdx.x + H, y = threadIdx.y + H;
+      float a3 = 0.f, a2 = 0.f, a1 = 0.f;
+#pragma unroll
+      for (int q = 1; q <= 4; ++q) {
+        a3 += w.c[q - 1] * (t[NR - 1][b][y][x + q] - t[NR - 1][b][y][x - q]);
+        a2 += w.c[q - 1] * (t[0][b][y + q][x] - t[0][b][y - q][x]);
+      }
+#pragma unroll
+      for (int q = 1; q <= 4; ++q) a1 += w.c[q - 1] * (win[H + q] - win[H - q]);
+      const size_t p = size_t(i) * g.plane + off;
+      if constexpr (DIV) {
+        float o = a1 * h1;  // out = d1 v1; += d2 v2; += d3 v3 (fd.cpp:171-177)
+        o += a2 * h2;
+        o += a3 * h3;
+        out[p] = o;
+      } else {
+        out[p] = a1 * h1;
+        out[N + p] = a2 * h2;
+        out[2 * N + p] = a3 * h3;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2 * H; ++q) win[q] = win[q + 1];
+    win[2 * H] = nxt;
+    nxt = nxt2;
+  }
+  fd_wait<0>();
 }
 
 FdGeo fd_geo(const Slab& s) {
@@ -200,14 +247,15 @@ int vreg_fd_grad(vreg_ctx ctx, const vreg_grid* gr, const float* f, float* out3)
     }
     Timed t(ctx, T_FD, "fd_grad");
     const FdGeo g = fd_geo(s);
-    const dim3 grid((s.n3 + TX - 1) / TX, (s.n2 + TY - 1) / TY, s.n1l), block(TX, TY);
+    const dim3 grid((s.n3 + TX - 1) / TX, (s.n2 + TY - 1) / TY, (s.n1l + FD_CH - 1) / FD_CH),
+        block(TX, TY);
     const float h1 = float(1.0 / s.h(0)), h2 = float(1.0 / s.h(1)), h3 = float(1.0 / s.h(2));
     if (dist)
-      k_fd_grad<true><<<grid, block, 0, ctx->stream>>>(g, f, gh.lo, gh.hi, fd_weights(), h1, h2,
-                                                       h3, out3);
+      k_fd_m<true, false><<<grid, block, 0, ctx->stream>>>(g, f, gh.lo, gh.hi, fd_weights(), h1,
+                                                         h2, h3, out3);
     else
-      k_fd_grad<false><<<grid, block, 0, ctx->stream>>>(g, f, nullptr, nullptr, fd_weights(), h1,
-                                                        h2, h3, out3);
+      k_fd_m<false, false><<<grid, block, 0, ctx->stream>>>(g, f, nullptr, nullptr, fd_weights(),
+                                                          h1, h2, h3, out3);
     count_launch(ctx);
     check_launch();
   });
@@ -225,14 +273,15 @@ int vreg_fd_div(vreg_ctx ctx, const vreg_grid* gr, const float* v3, float* out) 
     }
     Timed t(ctx, T_FD, "fd_div");
     const FdGeo g = fd_geo(s);
-    const dim3 grid((s.n3 + TX - 1) / TX, (s.n2 + TY - 1) / TY, s.n1l), block(TX, TY);
+    const dim3 grid((s.n3 + TX - 1) / TX, (s.n2 + TY - 1) / TY, (s.n1l + FD_CH - 1) / FD_CH),
+        block(TX, TY);
     const float h1 = float(1.0 / s.h(0)), h2 = float(1.0 / s.h(1)), h3 = float(1.0 / s.h(2));
     if (dist)
-      k_fd_div<true><<<grid, block, 0, ctx->stream>>>(g, v3, gh.lo, gh.hi, fd_weights(), h1, h2,
-                                                      h3, out);
+      k_fd_m<true, true><<<grid, block, 0, ctx->stream>>>(g, v3, gh.lo, gh.hi, fd_weights(), h1,
+                                                        h2, h3, out);
     else
-      k_fd_div<false><<<grid, block, 0, ctx->stream>>>(g, v3, nullptr, nullptr, fd_weights(), h1,
-                                                       h2, h3, out);
+      k_fd_m<false, true><<<grid, block, 0, ctx->stream>>>(g, v3, nullptr, nullptr, fd_weights(),
+                                                         h1, h2, h3, out);
     count_launch(ctx);
     check_launch();
   });

@@ -1,0 +1,20 @@
+"""Device time of fd_grad / fd_div at 256^3 (kernel timers)."""
+import torch
+
+from paper_2008_12820_b200.engine import Context
+
+ctx = Context(0)
+g = ctx.grid(256)
+f = torch.randn(256, 256, 256, device="cuda")
+v = torch.randn(3, 256, 256, 256, device="cuda")
+for _ in range(3):
+    ctx.fd_grad(g, f), ctx.fd_div(g, v)
+torch.cuda.synchronize()
+ctx.enable_timers(True)
+ctx.kernel_stats(reset=True)
+for _ in range(10):
+    ctx.fd_grad(g, f), ctx.fd_div(g, v)
+torch.cuda.synchronize()
+for k, s in ctx.kernel_stats().items():
+    us = s["seconds"] / s["count"] * 1e6
+    print(f"{k:10s} {us:8.1f} us  {16 * 256**3 / (us * 1e-6) / 1e9:7.0f} GB/s (16 B/voxel)")
