@@ -362,6 +362,114 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_gather_tile(
   }
 }
 
+// Tile-staged RK2 characteristics (engine.hpp:111-155). v changes with
+// every call, so each CTA derives its box from its own points' midpoint
+// displacements mid = -dt/h v (block min/max of the floors, as k_tile_boxes)
+// and then serves the three velocity components from one shared box in
+// turn: D_c = -(dt/2)/h_c (v_c + I[v_c](mid)). Tiles whose box exceeds the
+// budget take the per-point global path.
+template <int DEG, bool DIST>
+__global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_chars_tile(
+    Geo g, SrcField<DIST> s1, SrcField<DIST> s2, SrcField<DIST> s3, const float* __restrict__ v,
+    float m1, float m2, float m3, float c1, float c2, float c3, int box_cap_words,
+    float* __restrict__ D) {
+  constexpr int NN = DEG + 1, O0 = DEG == 3 ? -1 : 0;
+  extern __shared__ __align__(16) float fbox[];
+  __shared__ const float* rows[BOX_ROWS_MAX];
+  __shared__ int smn[3], smx[3];
+  __shared__ TileBox sb;
+  const int layer = blockIdx.z;
+  if (threadIdx.x < 3) {
+    smn[threadIdx.x] = 1 << 30;
+    smx[threadIdx.x] = -(1 << 30);
+  }
+  float va[TILE_PPT], vb[TILE_PPT], vc[TILE_PPT];
+  int mn[3] = {1 << 30, 1 << 30, 1 << 30}, mx[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
+#pragma unroll
+  for (int it = 0; it < TILE_PPT; ++it) {
+    TILE_PT(it)
+    va[it] = ok ? v[p] : 0.f;
+    vb[it] = ok ? v[g.N + p] : 0.f;
+    vc[it] = ok ? v[2 * g.N + p] : 0.f;
+    if (ok) {
+      const int f[3] = {int(floorf(m1 * va[it])), int(floorf(m2 * vb[it])),
+                        int(floorf(m3 * vc[it]))};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        mn[a] = min(mn[a], f[a]);
+        mx[a] = max(mx[a], f[a]);
+      }
+    }
+  }
+  __syncthreads();  // smn/smx initialised
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    mn[a] = __reduce_min_sync(0xffffffffu, mn[a]);
+    mx[a] = __reduce_max_sync(0xffffffffu, mx[a]);
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&smn[a], mn[a]);
+      atomicMax(&smx[a], mx[a]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // box of the tile (k_tile_boxes rules)
+    const int t[3] = {layer * TT1, int(blockIdx.y) * TT2, int(blockIdx.x) * TT3};
+    const int T[3] = {min(TT1, g.n1l - t[0]), min(TT2, g.n2 - t[1]), min(TT3, g.n3 - t[2])};
+    TileBox bx;
+    for (int a = 0; a < 3; ++a) {
+      bx.lo[a] = t[a] + smn[a] + O0;
+      bx.ext[a] = T[a] - 1 + (smx[a] - smn[a]) + NN;
+    }
+    if ((g.n3 & 3) == 0) {
+      const int sh = bx.lo[2] & 3;
+      bx.lo[2] -= sh;
+      bx.ext[2] = (bx.ext[2] + sh + 3) & ~3;
+    }
+    const int n[3] = {g.n1, g.n2, g.n3};
+    bool fits = smn[0] <= smx[0] && bx.ext[2] <= BOX_PITCH &&
+                bx.ext[0] * bx.ext[1] * BOX_PITCH <= box_cap_words;
+    for (int a = 0; a < 3; ++a)
+      fits = fits && bx.ext[a] <= n[a] && bx.lo[a] >= -n[a] && bx.lo[a] + bx.ext[a] <= 2 * n[a];
+    if (!fits) bx.ext[0] = -1;
+    sb = bx;
+  }
+  __syncthreads();
+  const TileBox b = sb;
+  const bool fits = b.ext[0] > 0;
+  const float cc[3] = {c1, c2, c3};
+#pragma unroll
+  for (int comp = 0; comp < 3; ++comp) {
+    const SrcField<DIST>& src = comp == 0 ? s1 : (comp == 1 ? s2 : s3);
+    if (fits) {
+      if (comp > 0) __syncthreads();  // previous component's gathers done
+      if (box_vec(g)) {
+        box_rows<DIST>(g, src, b, rows);
+        __syncthreads();
+      }
+      load_box(g, src, b, fbox, rows);
+      cp_async_wait_all();
+      __syncthreads();
+    }
+#pragma unroll
+    for (int it = 0; it < TILE_PPT; ++it) {
+      TILE_PT(it)
+      if (!ok) continue;
+      const float d1 = m1 * va[it], d2 = m2 * vb[it], d3 = m3 * vc[it];
+      float vs;
+      BoxStencil<DEG> bs;
+      if (fits && bs.build(b, i, j, k, d1, d2, d3))
+        vs = bs.gather(b, fbox);
+      else
+        vs = point_gather<DEG, DIST>(g, src, i, j, k, d1, d2, d3);
+      const float own = comp == 0 ? va[it] : (comp == 1 ? vb[it] : vc[it]);
+      D[size_t(comp) * g.N + p] = cc[comp] * (own + vs);
+    }
+  }
+}
+
 // Default transpose sweep: per-tile power-of-two scale S = 2^(27-e_tile)
 // in the shared int32 box (exact to 2^-28 max|z_tile| per contribution),
 // flushed with float4 REDs. The L2 adds of overlapping tiles land in any
@@ -1071,6 +1179,22 @@ int sl_characteristics(vreg_ctx ctx, const Slab& s, const float* v3, int degree,
   const float m1 = float(-dt / s.h(0)), m2 = float(-dt / s.h(1)), m3 = float(-dt / s.h(2));
   const float c1 = float(-0.5 * dt / s.h(0)), c2 = float(-0.5 * dt / s.h(1)),
               c3 = float(-0.5 * dt / s.h(2));
+  if (use_tile()) {
+    // box bound from max|v| (the midpoint floors spread by <= 2 floor(dt vmax / h) + 1)
+    int ext[3];
+    const int T[3] = {TT1, TT2, TT3};
+    for (int a = 0; a < 3; ++a)
+      ext[a] = T[a] + (degree == 3 ? 3 : 1) + 2 * int(std::floor(dt * vmax / s.h(a))) + 2;
+    ext[2] = ((ext[2] + 3 + 3) / 4) * 4;
+    const int words = std::min(BOX_CAP, ext[0] * ext[1] * BOX_PITCH);
+    const size_t smem = size_t(words) * sizeof(float);
+    SL_DISPATCH(degree, dist,
+                (tile_kernel(k_chars_tile<DEG, DIST>)<<<tile_grid(s), TILE_THREADS, smem,
+                                                        ctx->stream>>>(
+                    g, src_of<DIST>(v3, g1), src_of<DIST>(v3 + N, g2),
+                    src_of<DIST>(v3 + 2 * N, g3), v3, m1, m2, m3, c1, c2, c3, words, disp3)));
+    return 0;
+  }
   SL_DISPATCH(degree, dist,
               (k_characteristics<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
                   g, src_of<DIST>(v3, g1), src_of<DIST>(v3 + N, g2),
