@@ -307,7 +307,8 @@ __device__ __forceinline__ float tile_gather(const Geo& g, const SrcField<DIST>&
 
 // Gather kernels: issue the box as cp.async, prefetch the 8 points'
 // displacements meanwhile, then serve all taps from smem.
-template <int DEG, bool DIST, int MODE>  // MODE 0: interp(*q), 1: inc-state step
+template <int DEG, bool DIST, int MODE>  // MODE 0: interp(*q), 1: inc-state step,
+                                         // 2: inc-state step on precomputed u, 3: source factor
 __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_gather_tile(
     Geo g, SrcField<DIST> src, const int* __restrict__ boxes, const float* __restrict__ D,
     const float* __restrict__ qf, float* __restrict__ out, const float* __restrict__ vt,
@@ -349,6 +350,8 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_gather_tile(
       G = point_gather<DEG, DIST>(g, src, i, j, k, d1[it], d2[it], d3[it]);
     if constexpr (MODE == 0) {
       out[p] = qf ? G * qf[p] : G;
+    } else if constexpr (MODE == 3) {  // adjoint source factor (transport.hpp:55-60)
+      out[p] = (1.0f + half * G) / (1.0f - half * qf[p]);
     } else {
       float u;
       if constexpr (MODE == 2)
@@ -1213,6 +1216,15 @@ void sl_source_factor(vreg_ctx ctx, const Slab& s, const float* d, const float* 
   const Geo g = geo_of(s);
   const dim3 grid = sl_grid(s), block(BX, BY);
   const float half = float(0.5 * s.dt());
+  if (use_tile() && !ci.identity) {
+    const TileLaunch tl = tile_table(ctx, s, disp_bwd3, degree, false);
+    SL_DISPATCH(degree, dist,
+                (tile_kernel(k_gather_tile<DEG, DIST, 3>)<<<tile_grid(s), TILE_THREADS, tl.smem,
+                                                             ctx->stream>>>(
+                    g, src_of<DIST>(d, gh), tl.boxes, disp_bwd3, d, q, nullptr, nullptr, half, 0,
+                    nullptr, kAllLayers)));
+    return;
+  }
   SL_DISPATCH(degree, dist,
               (k_source_factor<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
                   g, src_of<DIST>(d, gh), disp_bwd3, ci.identity ? 1 : 0, half, q)));
