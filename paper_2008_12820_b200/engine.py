@@ -10,6 +10,7 @@ vector = (3, n1_local, n2, n3); characteristics = (disp (3, ...), flags).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 
 import torch
 
@@ -43,6 +44,7 @@ class Context:
             buf = C.create_string_buffer(bytes(uid), 128)
             check(lib().vreg_ctx_create_dist(device, rank, nranks, buf, C.byref(h)))
         self.h = h
+        self._dependents = weakref.WeakSet()  # solvers on this context: closed first
         self.rank, self.nranks = rank, nranks
         # order our kernels on torch's stream so tensor ops and ours interleave safely
         check(lib().vreg_ctx_set_stream(self.h, C.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
@@ -55,6 +57,8 @@ class Context:
 
     def close(self):
         if getattr(self, "h", None):
+            for d in list(getattr(self, "_dependents", ())):
+                d.close()
             lib().vreg_ctx_destroy(self.h)
             self.h = None
 

@@ -121,10 +121,14 @@ class Solver:
         h = C.c_void_p()
         check(lib().vreg_solver_create(ctx.h, C.byref(self.grid), C.byref(self._c), C.byref(h)))
         self.h = h
+        ctx._dependents.add(self)
 
     def close(self):
+        # a solver's device state lives in its context: destroy it while the
+        # context is open (Context.close closes its solvers first)
         if getattr(self, "h", None):
-            lib().vreg_solver_destroy(self.h)
+            if getattr(self.ctx, "h", None):
+                lib().vreg_solver_destroy(self.h)
             self.h = None
 
     def __del__(self):

@@ -187,3 +187,24 @@ def test_report_rendering_is_deterministic(ctx):
     assert rows[0] == "level,beta,gn_iter,pcg_iter,rel_residual"
     assert len(rows) - 1 == int(rep["total_pcg"]) + int(rep["total_gn"])  # + initial residuals
     assert t1.startswith("phases_s total")
+
+
+@pytest.mark.parametrize("shape", [(24, 20, 28), (18, 22, 26), (40, 16, 36)])
+def test_matvec_on_irregular_grids(ctx, shape):
+    """Non power-of-two and n3 % 4 != 0 grids: the regulariser falls back to
+    cuFFT, tile boxes to 4-byte rows, partial tiles along every axis."""
+    m0, v, m1 = ref.syn(shape)
+    cfg = Config(continuation=False, beta_target=BETA)
+    s = Solver(ctx, shape, cfg)
+    s.set_images(dev(m0), dev(m1))
+    s.linearize(dev(0.5 * v), BETA)
+    r = ref.Session(m0, m1, 0.5 * v, BETA, ref.Config(continuation=False, beta_target=BETA))
+    assert abs(s.objective()["total"] / r.objective()["total"] - 1) < 1e-5
+    g = r.gradient()
+    assert rel(host(s.gradient()), g) < 1e-5
+    assert rel(host(s.matvec(dev(-g))), r.matvec(-g)) < 1e-5
+    # two-level needs an even coarse grid (grid.hpp:19-26 on n/2)
+    p, _ = s.precond("2linvh0", dev(-g), 0.5) if all(n % 4 == 0 for n in shape) else (None, None)
+    if p is not None:
+        ref_p, _ = r.precond("2linvh0", -g, 0.5)
+        assert rel(host(p), ref_p) < 1e-4
