@@ -121,3 +121,26 @@ def test_hessian_symmetry(pair, ctx):
     a = ctx.inner(d.g, u, d.matvec(w))
     b = ctx.inner(d.g, d.matvec(u), w)
     assert abs(a - b) <= 1e-5 * max(abs(a), abs(b))
+
+
+def test_deterministic_mode_is_bitwise_reproducible(ctx):
+    """vreg_ctx_set_deterministic: exact fixed-point transpose sweeps give
+    bit-identical matvecs run to run, within fp32 round-off of the default
+    (fp32 L2 reductions) path."""
+    from paper_2008_12820_b200.solver import Config, Solver
+    n = 48
+    s = Solver(ctx, n, Config(continuation=False, beta_target=1e-3))
+    s.syn_images()
+    v = (0.5 * ctx.syn_velocity(s.grid)).contiguous()
+    s.linearize(v, 1e-3)
+    vt = (-s.gradient()).contiguous()
+    ctx.set_deterministic(True)
+    try:
+        a = s.matvec(vt).clone()
+        b = s.matvec(vt).clone()
+    finally:
+        ctx.set_deterministic(False)
+    c = s.matvec(vt)
+    assert torch.equal(a, b)
+    assert float((a - c).norm() / c.norm()) < 1e-6
+    s.close()
