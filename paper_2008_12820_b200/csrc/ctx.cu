@@ -170,13 +170,7 @@ static void init_ctx(vreg_ctx c, int device) {
   VB_CUDA(cudaSetDevice(device));
   VB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;
-  {
-    const char* e = std::getenv("VREG_SIDE_PRIO");  // diagnostics: "high" side stream
-    int lo = 0, hi = 0;
-    VB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    VB_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking,
-                                         (e && e[0] == 'h') ? hi : lo));
-  }
+  VB_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   {
     int lo = 0, hi = 0;
     VB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));

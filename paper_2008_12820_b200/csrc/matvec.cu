@@ -59,22 +59,15 @@ void gn_matvec(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int d
     sl_assemble(ctx, s, 1, psi, grads, reg, out3);
     return;
   }
-  // VREG_REGOP_FORK: 0 = overlap the inc-state steps (default), 1 = overlap
-  // the transpose sweeps (diagnostics)
-  static const int fork_at = [] {
-    const char* e = std::getenv("VREG_REGOP_FORK");
-    return e ? std::atoi(e) : 0;
-  }();
-  auto fork = [&] {
-    VB_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
-    VB_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+  // (overlapping the transpose sweeps instead measured slower)
+  VB_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
+  VB_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+  {
     SideRoute route(ctx);
     spectral_regop(ctx, s, vt3, beta, false, false, reg);
     VB_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
-  };
-  if (fork_at == 0) fork();
+  }
   sl_inc_state(ctx, s, disp3, flags, degree, grads, vt3, nullptr, psi + size_t(s.nt) * N);
-  if (fork_at == 1) fork();
   sl_transpose_sweeps(ctx, s, disp3, flags, degree, psi);
   VB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
   sl_assemble(ctx, s, 1, psi, grads, reg, out3);

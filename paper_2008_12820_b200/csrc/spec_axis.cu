@@ -508,11 +508,7 @@ bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, 
     return e && e[0] == '1';
   }();
   if (off) return false;
-  // VREG_AXIS_CTAS=k caps the grid at k CTAs per SM (persistent sweep)
-  static const int cap = [] {
-    const char* e = std::getenv("VREG_AXIS_CTAS");
-    return e ? std::atoi(e) : 0;
-  }();
+  const int cap = 0;  // one tile per CTA (a persistent cap measured slower)
   const AxisGeom loc{s.n1l, s.n2, s.n3};
   const double* sums = nullptr;
   if (unit_zero) {  // symbol beta at k = 0: + beta * mean(v_c) (spectral.cpp:48-70)
