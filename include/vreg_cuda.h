@@ -62,6 +62,9 @@ int vreg_ctx_create_dist(int device, int rank, int nranks, const void* uid128,
                          vreg_ctx* out);
 int vreg_ctx_destroy(vreg_ctx ctx);
 int vreg_ctx_rank(vreg_ctx ctx, int* rank, int* nranks);
+/* Pre-grow the device memory pool by up to `bytes` (capped at half the free
+ * memory) so later allocations do not map fresh pages mid-solve. */
+int vreg_ctx_reserve(vreg_ctx ctx, size_t bytes);
 /* Transpose (scatter) sweeps in exact fixed point: bitwise reproducible and
  * independent of the GPU count, ~10% slower matvec. Default off (fp32 L2
  * reductions, run-to-run differences in the last bits); env VREG_DETERMINISTIC=1. */

@@ -34,6 +34,7 @@ _SIGS = {
     "vreg_ctx_set_stream": (I, [VP, VP]),
     "vreg_ctx_get_stream": (I, [VP, C.POINTER(VP)]),
     "vreg_ctx_set_deterministic": (I, [VP, I]),
+    "vreg_ctx_reserve": (I, [VP, C.c_size_t]),
     "vreg_two_level_begin": (I, [VP, C.POINTER(VregGrid), VP, C.c_double, VP, VP]),
     "vreg_two_level_end": (I, [VP, C.POINTER(VregGrid), VP, VP]),
     "vreg_volume_save": (I, [C.c_char_p, I, I, I, I, I, VP]),

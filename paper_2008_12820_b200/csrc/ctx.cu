@@ -1,6 +1,7 @@
 // Context lifecycle, pooled memory, workspace cache, FFT plan cache, kernel
 // timers and slab distribution (EngineState analogue, engine.hpp:14-19;
 // FftPlanCache, fft.cpp:66-72; from_global/to_global, engine.hpp:63-66).
+#include <algorithm>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -266,6 +267,22 @@ int vreg_ctx_rank(vreg_ctx ctx, int* rank, int* nranks) {
   if (rank) *rank = ctx->rank;
   if (nranks) *nranks = ctx->nranks;
   return VREG_OK;
+}
+
+int vreg_ctx_reserve(vreg_ctx ctx, size_t bytes) {
+  return guard([&] {
+    // grow the stream-ordered pool once (its release threshold keeps the
+    // pages): mapping fresh device memory inside a solve costs ~0.1 s per
+    // few GB and showed up as random per-phase spikes in the registration
+    size_t free_b = 0, total_b = 0;
+    VB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    bytes = std::min(bytes, free_b / 2);
+    if (bytes == 0) return;
+    void* p = nullptr;
+    VB_CUDA(cudaMallocAsync(&p, bytes, ctx->stream));
+    VB_CUDA(cudaFreeAsync(p, ctx->stream));
+    VB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
 }
 
 int vreg_ctx_set_deterministic(vreg_ctx ctx, int on) {

@@ -162,6 +162,10 @@ int vreg_solver_create(vreg_ctx ctx, const vreg_grid* g, const vreg_config* cfg,
     s->eng = CudaEngine::create(grid, s->dev);
     s->m0 = s->eng.make_field();
     s->m1 = s->eng.make_field();
+    // working set of a solve, twice the paper's estimate (74 + nt) N mu0 / p
+    // (SPEC.md:384-386), reserved in the pool up front
+    const double n_local = double(g->n1) * g->n2 * g->n3 / double(s->eng.workers());
+    check(vreg_ctx_reserve(ctx, size_t(2.0 * (74 + s->cfg.nt) * n_local * sizeof(float))));
     *out = s.release();
   });
 }
