@@ -268,6 +268,7 @@ def run_ours(args):
     l0 = ctx.launches()
     ctx.enable_timers(True)
     t_before = ctx.timers()
+    c_before = ctx.comm()
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
@@ -280,6 +281,7 @@ def run_ours(args):
     ctx.enable_timers(False)
     kstats = ctx.kernel_stats()
     t_after = ctx.timers()
+    c_after = ctx.comm()
 
     t = torch.tensor([ms], device="cuda", dtype=torch.float64)
     if world > 1:
@@ -421,6 +423,18 @@ def run_ours(args):
                                        "ours_moved": bytes_per_voxel_ours(NT)},
             "matvec_frac_of_hbm": matvec_bytes / (ms / args.steps * 1e-3) / 1e9 / peak,
             "fft_ms_per_step": fft_s / args.steps * 1e3,
+            "nvlink": None if world == 1 else {
+                # bytes each GPU sends per matvec (halos, reverse halos, regulariser
+                # transposes) and the NVLink 5 time they would take alone
+                "bytes_per_matvec": sum(c_after[k] - c_before[k] for k in (
+                    "ghost_interp_bytes", "scatter_points_bytes", "fft_transpose_bytes",
+                    "ghost_fd_bytes", "reduce_bytes")) / args.steps,
+                "peak_gbs_per_direction": 900.0,
+                "ms_at_peak": sum(c_after[k] - c_before[k] for k in (
+                    "ghost_interp_bytes", "scatter_points_bytes", "fft_transpose_bytes",
+                    "ghost_fd_bytes", "reduce_bytes")) / args.steps / 900e9 * 1e3,
+                "comm_timer_ms": round(sum((t_after[k] - t_before[k]) for k in (
+                    "interp_comm", "scatter_comm", "transpose_comm")) / args.steps * 1e3, 4)},
             "timer_ms_per_step": {k: round((t_after[k] - t_before[k]) / args.steps * 1e3, 4)
                                   for k in t_after if t_after[k] != t_before[k]},
             "kernel_share": share,
