@@ -22,11 +22,21 @@ struct SpecDesc {
   size_t nc;          // local complex elements per component
 };
 
-__device__ __forceinline__ void spec_index(const SpecDesc& d, size_t e, int& k1, int& k2, int& k3) {
-  k3 = int(e % size_t(d.h));
-  const size_t r = e / size_t(d.h);
-  k2 = int(r % size_t(d.n2l)) + d.k2off;
-  k1 = int(r / size_t(d.n2l));
+// 32-bit index arithmetic: a GPU's spectra stay below 2^32 elements, and
+// 64-bit div/mod (~100 instructions each) dominated these streaming passes.
+__device__ __forceinline__ void spec_index(const SpecDesc& d, unsigned e, int& k1, int& k2, int& k3) {
+  k3 = int(e % unsigned(d.h));
+  const unsigned r = e / unsigned(d.h);
+  k2 = int(r % unsigned(d.n2l)) + d.k2off;
+  k1 = int(r / unsigned(d.n2l));
+}
+
+__device__ __forceinline__ void split3(unsigned r, unsigned h, unsigned n2, int& k1, int& k2,
+                                       int& k3) {
+  k3 = int(r % h);
+  const unsigned q = r / h;
+  k2 = int(q % n2);
+  k1 = int(q / n2);
 }
 
 __device__ __forceinline__ float sfreq(int k, int n) { return float(k <= n / 2 ? k : k - n); }
@@ -39,13 +49,14 @@ constexpr unsigned kT = 256;
 // 1 / (beta |k|^2) (zero mode 1/beta) [inv_regop] (spectral.cpp:48-93).
 __global__ void k_symbol(SpecDesc d, int ncomp, float2* __restrict__ F, float beta, int inverse,
                          int unit_zero, float scale) {
-  const size_t total = d.nc * size_t(ncomp);
-  const size_t stride = size_t(gridDim.x) * blockDim.x;
-  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
-    int k1, k2, k3;
-    spec_index(d, e % d.nc, k1, k2, k3);
-    const float f1 = sfreq(k1, d.n1), f2 = sfreq(k2, d.n2), f3 = float(k3);
-    float sym = f1 * f1 + f2 * f2 + f3 * f3;
+  // one CTA per (component, k1, local k2) row, threads along k3
+  const int k2l = blockIdx.x, c = blockIdx.y / d.n1, k1 = blockIdx.y - c * d.n1;
+  const float f1 = sfreq(k1, d.n1), f2 = sfreq(k2l + d.k2off, d.n2);
+  const float f12 = f1 * f1 + f2 * f2;
+  float2* R = F + size_t(c) * d.nc + (size_t(k1) * d.n2l + k2l) * d.h;
+  for (int k3 = threadIdx.x; k3 < d.h; k3 += blockDim.x) {
+    const float f3 = float(k3);
+    float sym = f12 + f3 * f3;
     float m;
     if (inverse) {
       if (sym == 0.0f) sym = 1.0f;
@@ -54,17 +65,17 @@ __global__ void k_symbol(SpecDesc d, int ncomp, float2* __restrict__ F, float be
       if (sym == 0.0f) sym = unit_zero ? 1.0f : 0.0f;
       m = scale * (beta * sym);
     }
-    float2 v = F[e];
+    float2 v = R[k3];
     v.x *= m;
     v.y *= m;
-    F[e] = v;
+    R[k3] = v;
   }
 }
 
 // Leray: F_c -= f_c (f . F)/|k|^2, zero mode untouched (spectral.cpp:120-147).
 __global__ void k_leray(SpecDesc d, float2* __restrict__ F, float scale) {
-  const size_t stride = size_t(gridDim.x) * blockDim.x;
-  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < d.nc; e += stride) {
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < unsigned(d.nc); e += stride) {
     int k1, k2, k3;
     spec_index(d, e, k1, k2, k3);
     const float f1 = sfreq(k1, d.n1), f2 = sfreq(k2, d.n2), f3 = float(k3);
@@ -134,12 +145,13 @@ __global__ void k_restrict(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3,
                            const float2* __restrict__ Ff, float2* __restrict__ Fc, float scale) {
   const int hc = nc3 / 2 + 1, hf = nf3 / 2 + 1;
   const size_t ncc = size_t(nc1) * nc2 * hc, ncf = size_t(nf1) * nf2 * hf;
-  const size_t total = ncc * size_t(ncomp);
-  const size_t stride = size_t(gridDim.x) * blockDim.x;
-  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int c = int(e / ncc);
-    const size_t r = e % ncc;
-    const int k3 = int(r % hc), k2 = int((r / hc) % nc2), k1 = int(r / (size_t(hc) * nc2));
+  const unsigned total = unsigned(ncc) * unsigned(ncomp);
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int c = int(e / unsigned(ncc));
+    const unsigned r = e - unsigned(c) * unsigned(ncc);
+    int k1, k2, k3;
+    split3(r, unsigned(hc), unsigned(nc2), k1, k2, k3);
     const int nu1 = k1 <= nc1 / 2 ? k1 : k1 - nc1;
     const int nu2 = k2 <= nc2 / 2 ? k2 : k2 - nc2;
     const int nu3 = k3;
@@ -184,12 +196,13 @@ __global__ void k_prolong(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3, 
                           const float2* __restrict__ Fc, float2* __restrict__ Ff, float scale) {
   const int hc = nc3 / 2 + 1, hf = nf3 / 2 + 1;
   const size_t ncc = size_t(nc1) * nc2 * hc, ncf = size_t(nf1) * nf2 * hf;
-  const size_t total = ncf * size_t(ncomp);
-  const size_t stride = size_t(gridDim.x) * blockDim.x;
-  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int c = int(e / ncf);
-    const size_t r = e % ncf;
-    const int f3 = int(r % hf), f2 = int((r / hf) % nf2), f1 = int(r / (size_t(hf) * nf2));
+  const unsigned total = unsigned(ncf) * unsigned(ncomp);
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int c = int(e / unsigned(ncf));
+    const unsigned r = e - unsigned(c) * unsigned(ncf);
+    int f1, f2, f3;
+    split3(r, unsigned(hf), unsigned(nf2), f1, f2, f3);
     Ff[e] = prolong_elem(nf1, nf2, nc1, nc2, nc3, Fc + size_t(c) * ncc, f1, f2, f3, scale);
   }
 }
@@ -233,29 +246,32 @@ __global__ void k_high_pass(int n1, int n2, int n3, int ncomp, const float2* __r
                             float2* __restrict__ Fout, float scale) {
   const int h = n3 / 2 + 1;
   const size_t nc = size_t(n1) * n2 * h;
-  const size_t total = nc * size_t(ncomp);
-  const size_t stride = size_t(gridDim.x) * blockDim.x;
-  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int c = int(e / nc);
-    const size_t r = e % nc;
-    const int k3 = int(r % h), k2 = int((r / h) % n2), k1 = int(r / (size_t(h) * n2));
+  const unsigned total = unsigned(nc) * unsigned(ncomp);
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int c = int(e / unsigned(nc));
+    const unsigned r = e - unsigned(c) * unsigned(nc);
+    int k1, k2, k3;
+    split3(r, unsigned(h), unsigned(n2), k1, k2, k3);
     Fout[e] = high_pass_elem(n1, n2, n3, Fin + size_t(c) * nc, k1, k2, k3, scale);
   }
 }
 
 // Fused end of the two-level apply: G = prolong(Fc) + high_pass(Ff) on the
-// fine half spectrum (3-D grid: k3 over x, k2 over y, (comp, k1) over z).
+// fine half spectrum. One CTA per (component, k1, k2) row, threads along k3:
+// no index division at all.
 __global__ void k_prolong_plus_hp(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3,
                                   const float2* __restrict__ Fc, const float2* __restrict__ Ff,
                                   float2* __restrict__ G, float scale_p, float scale_h) {
   const int hf = nf3 / 2 + 1, hc = nc3 / 2 + 1;
-  const int k3 = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k3 >= hf) return;
-  const int k2 = blockIdx.y, c = blockIdx.z / nf1, k1 = blockIdx.z - c * nf1;
+  const int k2 = blockIdx.x, c = blockIdx.y / nf1, k1 = blockIdx.y - c * nf1;
   const size_t ncf = size_t(nf1) * nf2 * hf, ncc = size_t(nc1) * nc2 * hc;
-  const float2 a = prolong_elem(nf1, nf2, nc1, nc2, nc3, Fc + c * ncc, k1, k2, k3, scale_p);
-  const float2 b = high_pass_elem(nf1, nf2, nf3, Ff + c * ncf, k1, k2, k3, scale_h);
-  G[c * ncf + (size_t(k1) * nf2 + k2) * hf + k3] = make_float2(a.x + b.x, a.y + b.y);
+  const size_t row = size_t(c) * ncf + (size_t(k1) * nf2 + k2) * hf;
+  for (int k3 = threadIdx.x; k3 < hf; k3 += blockDim.x) {
+    const float2 a = prolong_elem(nf1, nf2, nc1, nc2, nc3, Fc + c * ncc, k1, k2, k3, scale_p);
+    const float2 b = high_pass_elem(nf1, nf2, nf3, Ff + c * ncf, k1, k2, k3, scale_h);
+    G[row + k3] = make_float2(a.x + b.x, a.y + b.y);
+  }
 }
 
 // out_c += g_c (g . s) (precond.hpp:36-37)
@@ -284,6 +300,7 @@ SpecDesc spec_desc(vreg_ctx ctx, const Slab& s) {
   d.n2l = s.n2 / ctx->nranks;
   d.k2off = ctx->rank * d.n2l;
   d.nc = size_t(s.n1) * d.n2l * d.h;
+  require(3 * d.nc < (size_t(1) << 32), VREG_EDIM, "spectrum too large for 32-bit indexing");
   return d;
 }
 
@@ -321,7 +338,7 @@ void fft_inverse(vreg_ctx ctx, const Slab& s, int ncomp, float2* F, float* f) {
 void apply_symbol(vreg_ctx ctx, const SpecDesc& d, int ncomp, float2* F, double beta, bool inverse,
                   bool unit_zero, double scale) {
   Timed t(ctx, T_FFT, "spec_symbol");
-  k_symbol<<<blocks_for(d.nc * ncomp, kT), kT, 0, ctx->stream>>>(
+  k_symbol<<<dim3(unsigned(d.n2l), unsigned(ncomp * d.n1)), 128, 0, ctx->stream>>>(
       d, ncomp, F, float(beta), inverse ? 1 : 0, unit_zero ? 1 : 0, float(scale));
   count_launch(ctx);
   check_launch();
@@ -543,8 +560,7 @@ int vreg_two_level_end(vreg_ctx ctx, const vreg_grid* g, const float* sc3, float
     float2* Fc = spec_buffer(ctx, dc, 3, "tl_Fc");
     float2* G = spec_buffer(ctx, df, 3, "tl_G");
     fft_forward(ctx, sc, 3, sc3, Fc);
-    const dim3 grid(unsigned((df.h + 127) / 128), unsigned(s.n2), unsigned(3 * s.n1));
-    k_prolong_plus_hp<<<grid, 128, 0, ctx->stream>>>(
+    k_prolong_plus_hp<<<dim3(unsigned(s.n2), unsigned(3 * s.n1)), 128, 0, ctx->stream>>>(
         s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, Fc, F, G, float(1.0 / double(sc.global())),
         float(1.0 / double(s.global())));
     count_launch(ctx);
