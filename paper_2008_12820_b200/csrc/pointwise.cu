@@ -90,11 +90,30 @@ __global__ void k_plane_partials(const float* __restrict__ a, const float* __res
   size_t end = beg + chunk_len;
   if (end > (pl + 1) * plane) end = (pl + 1) * plane;
   double acc = 0.0;
-  for (size_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
-    if (kMax) {
-      acc = fmax(acc, fabs(double(a[i])));
-    } else {
-      acc += double(a[i]) * double(b[i]);
+  if (((beg | end) & 3) == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0) {
+    // 16-byte lanes (uniform per block): same element set, 4x fewer loads
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    for (size_t i = beg / 4 + threadIdx.x; i < end / 4; i += blockDim.x) {
+      const float4 x = a4[i];
+      if (kMax) {
+        acc = fmax(fmax(fmax(fmax(acc, fabs(double(x.x))), fabs(double(x.y))), fabs(double(x.z))),
+                   fabs(double(x.w)));
+      } else {
+        const float4 y = b4[i];
+        acc += double(x.x) * double(y.x);
+        acc += double(x.y) * double(y.y);
+        acc += double(x.z) * double(y.z);
+        acc += double(x.w) * double(y.w);
+      }
+    }
+  } else {
+    for (size_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+      if (kMax) {
+        acc = fmax(acc, fabs(double(a[i])));
+      } else {
+        acc += double(a[i]) * double(b[i]);
+      }
     }
   }
   __shared__ double sh[kThreads];
