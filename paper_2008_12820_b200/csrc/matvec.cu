@@ -17,6 +17,7 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
                   const float* grads, const float* vt3, float* mt_all, float* psi_out);
 void sl_transpose_sweeps(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int degree,
                          float* psi);
+float* sl_matvec_psi(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int degree);
 void sl_assemble(vreg_ctx ctx, const Slab& s, int descending, const float* sl, const float* grads,
                  const float* reg, float* out3);
 void spectral_regop(vreg_ctx ctx, const Slab& s, const float* v3, double beta, bool unit_zero,
@@ -46,7 +47,7 @@ struct SideRoute {
 void gn_matvec(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int degree,
                const float* grads, double beta, const float* vt3, float* out3) {
   const size_t N = s.local();
-  float* psi = static_cast<float*>(workspace(ctx, "mv_psi", size_t(s.nt + 1) * N * sizeof(float)));
+  float* psi = sl_matvec_psi(ctx, s, disp3, flags, degree);
   float* reg = static_cast<float*>(workspace(ctx, "mv_reg", 3 * N * sizeof(float)));
   static const bool serial = [] {  // diagnostics: VREG_SERIAL_MATVEC=1 -> no overlap
     const char* e = std::getenv("VREG_SERIAL_MATVEC");

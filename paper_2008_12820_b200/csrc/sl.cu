@@ -933,6 +933,22 @@ inline CharsInfo chars_info(vreg_ctx ctx, const Slab& s, const float* disp3, int
   return ci;
 }
 
+// Fused peer-memory sweeps (p2p.cu, VREG_P2P_SL=1): w and psi live in the
+// IPC arena, the tile kernels read ghost planes from / add ghost
+// contributions into the neighbours' copies directly.
+inline bool p2p_sweeps(vreg_ctx ctx, const Slab& s, const CharsInfo& ci) {
+  return ctx->nranks > 1 && !ci.identity && use_tile() && !ctx->deterministic &&
+         s.local() % 4 == 0 && ci.G >= 1 && ci.G <= s.n1l && p2p_enabled(ctx);
+}
+inline bool in_arena(vreg_ctx ctx, const void* p) {
+  const char* c = static_cast<const char*>(p);
+  return ctx->parena && c >= ctx->parena && c < ctx->parena + ctx->parena_bytes;
+}
+template <class T>
+inline T* peer_plane(vreg_ctx ctx, T* local, bool next, size_t plane_off) {
+  return reinterpret_cast<T*>(const_cast<char*>(p2p_peer(ctx, local, next))) + plane_off;
+}
+
 // out = I[f] at disp (optionally .* q)
 void interp_sweep(vreg_ctx ctx, const Slab& s, const float* f, const float* disp3,
                   const CharsInfo& ci, int degree, const float* q, float* out) {
@@ -1092,10 +1108,16 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
   const size_t N = s.local();
   const int nt = s.nt;
   const float half = float(0.5 * s.dt());
-  float* w = static_cast<float*>(workspace(ctx, "inc_w", 2 * N * sizeof(float)));
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
   // tile path: all u_t in one streaming pass, steps then read one float each
   const bool fused_u = use_tile() && !ci.identity && N % 4 == 0 && al16(vt3) && al16(grads);
+  // peer-memory steps: w_t in the arena (its first 2N floats), the
+  // neighbours read their ghost planes from it (sl_matvec_psi placed psi there)
+  const bool p2p = fused_u && in_arena(ctx, psi_out) && p2p_sweeps(ctx, s, ci);
+  float* w = p2p ? reinterpret_cast<float*>(p2p_data(ctx, size_t(nt + 3) * N * sizeof(float)))
+                 : static_cast<float*>(workspace(ctx, "inc_w", 2 * N * sizeof(float)));
+  // the neighbours finished reading my w slots in the previous solve
+  if (p2p && ctx->pdone) p2p_wait(ctx, P2P_DONE, ctx->pdone);
   float* u = fused_u ? static_cast<float*>(workspace(ctx, "inc_u", size_t(nt) * N * sizeof(float)))
                      : nullptr;
   {
@@ -1122,7 +1144,31 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
     if (dist && !use_tile())
       gh = halo_exchange(ctx, s, wt, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
     Timed tm(ctx, T_SL, "sl_inc_step");
-    if (fused_u) {
+    if (p2p) {
+      const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
+      const uint64_t ready = p2p_seq(ctx);
+      p2p_signal(ctx, P2P_READY, ready);            // my w_t is complete
+      if (t > 0 && !last) p2p_wait(ctx, P2P_DONE, ctx->pdone);  // wn's slot held w_{t-1}
+      gh.G = ci.G;
+      gh.lo = peer_plane(ctx, wt, false, size_t(s.n1l - ci.G) * s.plane());
+      gh.hi = peer_plane(ctx, wt, true, 0);
+      const LayerSplit ls = layer_split(s, ci.G);
+      auto launch = [&](TileZ zm, int nz) {
+        SL_DISPATCH(degree, true,
+                    (tile_kernel(k_gather_tile<DEG, DIST, 2>)<<<tile_grid_nz(s, nz), TILE_THREADS,
+                                                                 tl.smem, ctx->stream>>>(
+                        g, src_of<DIST>(wt, gh), tl.boxes, disp3, u + size_t(t) * N, wn, nullptr,
+                        nullptr, half, last ? 1 : 0, mo, zm)));
+      };
+      if (ls.on) launch(TileZ{ls.zb, 1 << 30, 0}, ls.ntz - 2 * ls.zb);  // interior first
+      p2p_wait(ctx, P2P_READY, ready);
+      if (ls.on)
+        launch(TileZ{0, ls.zb, ls.ntz - ls.zb}, 2 * ls.zb);
+      else
+        launch(kAllLayers, ls.ntz);
+      ctx->pdone = p2p_seq(ctx);
+      p2p_signal(ctx, P2P_DONE, ctx->pdone);        // done reading the neighbours' w_t
+    } else if (fused_u) {
       const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
       gather_tiles(ctx, s, wt, ci.G, dist, gh, [&](TileZ zm, int nz) {
         SL_DISPATCH(degree, dist,
@@ -1170,9 +1216,57 @@ void sl_transpose_sweeps(vreg_ctx ctx, const Slab& s, const float* disp3, int fl
     count_launch(ctx);
     check_launch();
   }
+  if (in_arena(ctx, psi) && p2p_sweeps(ctx, s, ci)) {
+    // each sweep: zero my slice, handshake, boundary tiles add straight into
+    // the neighbours' slices, interior tiles, then wait for their adds
+    const Geo g = geo_of(s);
+    const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
+    const LayerSplit ls = layer_split(s, ci.G);
+    for (int t = s.nt; t > 0; --t) {
+      Timed tm(ctx, T_SL, "sl_scatter_sweep");
+      const float* z = psi + size_t(t) * N;
+      float* out = psi + size_t(t - 1) * N;
+      VB_CUDA(cudaMemsetAsync(out, 0, N * sizeof(float), ctx->stream));
+      const uint64_t zeroed = p2p_seq(ctx);
+      p2p_signal(ctx, P2P_ZEROED, zeroed);
+      GhostAcc acc;
+      acc.G = ci.G;
+      acc.lo = peer_plane(ctx, out, false, size_t(s.n1l - ci.G) * s.plane());
+      acc.hi = peer_plane(ctx, out, true, 0);
+      auto launch = [&](TileZ zm, int nz) {
+        SL_DISPATCH(degree, true,
+                    (tile_kernel(k_scatter_tile_fp<DEG, DIST>)<<<tile_grid_nz(s, nz),
+                                                                 TILE_THREADS, tl.smem,
+                                                                 ctx->stream>>>(
+                        g, dst_of<DIST>(out, acc), tl.boxes, disp3, z, zm)));
+      };
+      p2p_wait(ctx, P2P_ZEROED, zeroed);
+      const uint64_t added = p2p_seq(ctx);
+      if (ls.on) {
+        launch(TileZ{0, ls.zb, ls.ntz - ls.zb}, 2 * ls.zb);
+        p2p_signal(ctx, P2P_ADDED, added);
+        launch(TileZ{ls.zb, 1 << 30, 0}, ls.ntz - 2 * ls.zb);
+      } else {
+        launch(kAllLayers, ls.ntz);
+        p2p_signal(ctx, P2P_ADDED, added);
+      }
+      p2p_wait(ctx, P2P_ADDED, added);
+    }
+    return;
+  }
   for (int t = s.nt; t > 0; --t)
     scatter_sweep(ctx, s, psi + size_t(t) * N, disp3, ci, degree, psi + size_t(t - 1) * N,
                   mx ? mx + t : nullptr, mx && t > 1 ? mx + t - 1 : nullptr);
+}
+
+// psi buffer ((nt+1) slices) of a GN matvec: the peer arena when the fused
+// peer-memory sweeps apply, else a workspace.
+float* sl_matvec_psi(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int degree) {
+  const size_t N = s.local();
+  const CharsInfo ci = chars_info(ctx, s, disp3, flags, degree);
+  if (p2p_sweeps(ctx, s, ci))
+    return reinterpret_cast<float*>(p2p_data(ctx, size_t(s.nt + 3) * N * sizeof(float))) + 2 * N;
+  return static_cast<float*>(workspace(ctx, "mv_psi", size_t(s.nt + 1) * N * sizeof(float)));
 }
 
 void sl_assemble(vreg_ctx ctx, const Slab& s, int descending, const float* sl,

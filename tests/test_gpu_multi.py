@@ -16,14 +16,15 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("nproc", [2, 4])
-def test_slab_decomposed_matches_single_gpu(nproc):
+@pytest.mark.parametrize("nproc,p2p", [(2, "0"), (4, "0"), (2, "1"), (4, "1")])
+def test_slab_decomposed_matches_single_gpu(nproc, p2p):
+    """p2p "1": the fused peer-memory SL sweeps (VREG_P2P_SL, p2p.cu)."""
     if torch.cuda.device_count() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
-    env = dict(os.environ, NCCL_DEBUG="WARN")
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+    env = dict(os.environ, NCCL_DEBUG="WARN", VREG_P2P_SL=p2p)
+    r = subprocess.run(["timeout", "600", sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
-                        f"--master-port={29600 + nproc}", os.path.join(ROOT, "tools", "mgpu_check.py"),
+                        f"--master-port={29600 + 10 * nproc + int(p2p)}", os.path.join(ROOT, "tools", "mgpu_check.py"),
                         "64"], capture_output=True, text=True, timeout=900, env=env)
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-2000:]
