@@ -65,6 +65,13 @@ int vreg_ctx_rank(vreg_ctx ctx, int* rank, int* nranks);
 /* Pre-grow the device memory pool by up to `bytes` (capped at half the free
  * memory) so later allocations do not map fresh pages mid-solve. */
 int vreg_ctx_reserve(vreg_ctx ctx, size_t bytes);
+/* Host-only: the x1 halo plan for ghost width G on slabs of n1l planes
+ * (G may exceed n1l: "wide" halos span several ranks; replaces the point
+ * routing of SPEC.md:513-520 for far departure points). Chunk i (i < return
+ * value <= cap) comes from the rank at ring distance d[i]: c[i] planes, the
+ * owner's last c[i] planes into the lo ghost at plane lo[i], its first c[i]
+ * planes into the hi ghost at plane hi[i]. Returns the chunk count, or -1. */
+int vreg_halo_chunks(int n1l, int G, int cap, int* d, int* c, long long* lo, long long* hi);
 /* Transpose (scatter) sweeps in exact fixed point: bitwise reproducible and
  * independent of the GPU count, ~10% slower matvec. Default off (fp32 L2
  * reductions, run-to-run differences in the last bits); env VREG_DETERMINISTIC=1. */

@@ -35,6 +35,8 @@ _SIGS = {
     "vreg_ctx_get_stream": (I, [VP, C.POINTER(VP)]),
     "vreg_ctx_set_deterministic": (I, [VP, I]),
     "vreg_ctx_reserve": (I, [VP, C.c_size_t]),
+    "vreg_halo_chunks": (I, [I, I, I, C.POINTER(I), C.POINTER(I), C.POINTER(C.c_longlong),
+                             C.POINTER(C.c_longlong)]),
     "vreg_two_level_begin": (I, [VP, C.POINTER(VregGrid), VP, C.c_double, VP, VP]),
     "vreg_two_level_end": (I, [VP, C.POINTER(VregGrid), VP, VP]),
     "vreg_volume_save": (I, [C.c_char_p, I, I, I, I, I, VP]),

@@ -8,7 +8,9 @@
 //    to x2 slabs, unpack, batched 1-D C2C along x1; inverse in
 //    reverse order;
 //  - all-gather of per-plane fp64 reduction partials (p-independent folds).
+#include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "common.cuh"
 
@@ -125,28 +127,61 @@ void alltoall_chunks(vreg_ctx ctx, const float2* send, float2* recv, size_t chun
 
 }  // namespace
 
+// Halo chunks for a ghost width G that may exceed the slab width n1l (wide
+// halos: large displacements or many ranks). Chunk d = 1..D, D = ceil(G/n1l),
+// comes from the rank at ring distance d and has c_d = min(n1l, G - (d-1) n1l)
+// planes: the owner's last c_d planes land in lo at plane G - (d-1) n1l - c_d,
+// its first c_d planes in hi at plane (d-1) n1l. D = 1 is the plain
+// neighbour halo. Per peer pair, messages are issued in d order with the
+// lo-bound one first on both sides, which is what NCCL's in-order matching
+// of same-peer send/recv needs (at p = 2, or d >= p, peers repeat).
+struct HaloChunk {
+  int d, c;
+  size_t lo_plane, hi_plane;
+};
+std::vector<HaloChunk> halo_chunks(int n1l, int G) {
+  std::vector<HaloChunk> v;
+  for (int d = 1; (d - 1) * n1l < G; ++d) {
+    const int c = std::min(n1l, G - (d - 1) * n1l);
+    v.push_back({d, c, size_t(G - (d - 1) * n1l - c), size_t(d - 1) * n1l});
+  }
+  return v;
+}
+
+namespace {
+// ncclSend/ncclRecv pair, or a device copy when the peer is this rank
+void xfer(vreg_ctx ctx, const float* src, float* dst, size_t n, int to, int from) {
+  if (to == ctx->rank) {
+    VB_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
+    return;
+  }
+  VB_NCCL(ncclSend(src, n, ncclFloat, to, ctx->comm, ctx->stream));
+  VB_NCCL(ncclRecv(dst, n, ncclFloat, from, ctx->comm, ctx->stream));
+}
+}  // namespace
+
 Ghosts halo_exchange(vreg_ctx ctx, const Slab& s, const float* f, int G, const char* slot,
                      int timer_cat, int comm_cat) {
-  require(G >= 1 && G <= s.n1l, VREG_ECONFIG,
-          "ghost width exceeds the slab width (reduce ranks or time step)");
-  const size_t gp = size_t(G) * s.plane();
+  require(G >= 1, VREG_ECONFIG, "ghost width must be positive");
+  const size_t gp = size_t(G) * s.plane(), pl = s.plane();
   std::string base(slot);
   float* lo = static_cast<float*>(workspace(ctx, base + "_lo", gp * sizeof(float)));
   float* hi = static_cast<float*>(workspace(ctx, base + "_hi", gp * sizeof(float)));
   Timed t(ctx, timer_cat);
-  const int p = ctx->nranks;
-  const int prev = (ctx->rank - 1 + p) % p, next = (ctx->rank + 1) % p;
-  const float* first = f;
-  const float* last = f + size_t(s.n1l - G) * s.plane();
+  const int p = ctx->nranks, r = ctx->rank;
+  const auto chunks = halo_chunks(s.n1l, G);
   VB_NCCL(ncclGroupStart());
-  // order per peer: the message that lands in the peer's lo goes first
-  VB_NCCL(ncclSend(last, gp, ncclFloat, next, ctx->comm, ctx->stream));
-  VB_NCCL(ncclSend(first, gp, ncclFloat, prev, ctx->comm, ctx->stream));
-  VB_NCCL(ncclRecv(lo, gp, ncclFloat, prev, ctx->comm, ctx->stream));
-  VB_NCCL(ncclRecv(hi, gp, ncclFloat, next, ctx->comm, ctx->stream));
+  for (const HaloChunk& h : chunks) {
+    const int fwd = (r + h.d) % p, bwd = ((r - h.d) % p + p) % p;
+    const size_t n = size_t(h.c) * pl;
+    // my last c planes -> lo of rank r+d; lo chunk from rank r-d
+    xfer(ctx, f + size_t(s.n1l - h.c) * pl, lo + h.lo_plane * pl, n, fwd, bwd);
+    // my first c planes -> hi of rank r-d; hi chunk from rank r+d
+    xfer(ctx, f, hi + h.hi_plane * pl, n, bwd, fwd);
+  }
   VB_NCCL(ncclGroupEnd());
   ctx->comm_bytes[comm_cat] += 2 * gp * sizeof(float);
-  ctx->comm_bytes[C_P2P_MSGS] += 2;
+  ctx->comm_bytes[C_P2P_MSGS] += 2 * chunks.size();
   Ghosts g;
   g.lo = lo;
   g.hi = hi;
@@ -155,8 +190,7 @@ Ghosts halo_exchange(vreg_ctx ctx, const Slab& s, const float* f, int G, const c
 }
 
 GhostAcc ghost_accumulators(vreg_ctx ctx, const Slab& s, int G, const char* slot) {
-  require(G >= 1 && G <= s.n1l, VREG_ECONFIG,
-          "ghost width exceeds the slab width (reduce ranks or time step)");
+  require(G >= 1, VREG_ECONFIG, "ghost width must be positive");
   const size_t gp = size_t(G) * s.plane();
   std::string base(slot);
   float* lo = static_cast<float*>(workspace(ctx, base + "_lo", gp * sizeof(float)));
@@ -173,56 +207,61 @@ GhostAcc ghost_accumulators(vreg_ctx ctx, const Slab& s, int G, const char* slot
   return a;
 }
 
+// Reverse halo: ghost accumulator chunks go back to their owners; the
+// received chunks keep the senders' offsets (top mirrors lo, bot mirrors hi).
 RevHalo halo_reverse_send(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, const char* slot) {
-  const size_t gp = size_t(acc.G) * s.plane();
+  const size_t gp = size_t(acc.G) * s.plane(), pl = s.plane();
   std::string base(slot);
   RevHalo r;
   r.top = static_cast<float*>(workspace(ctx, base + "_rtop", gp * sizeof(float)));
   r.bot = static_cast<float*>(workspace(ctx, base + "_rbot", gp * sizeof(float)));
   r.G = acc.G;
-  const int p = ctx->nranks;
-  const int prev = (ctx->rank - 1 + p) % p, next = (ctx->rank + 1) % p;
+  const int p = ctx->nranks, me = ctx->rank;
+  const auto chunks = halo_chunks(s.n1l, acc.G);
   Timed t(ctx, T_SCATTER_COMM);
   VB_NCCL(ncclGroupStart());
-  VB_NCCL(ncclSend(acc.lo, gp, ncclFloat, prev, ctx->comm, ctx->stream));
-  VB_NCCL(ncclSend(acc.hi, gp, ncclFloat, next, ctx->comm, ctx->stream));
-  VB_NCCL(ncclRecv(r.top, gp, ncclFloat, next, ctx->comm, ctx->stream));
-  VB_NCCL(ncclRecv(r.bot, gp, ncclFloat, prev, ctx->comm, ctx->stream));
+  for (const HaloChunk& h : chunks) {
+    const int fwd = (me + h.d) % p, bwd = ((me - h.d) % p + p) % p;
+    const size_t n = size_t(h.c) * pl;
+    // lo chunk -> its owner r-d; the owner-side copy arrives from r+d into top
+    xfer(ctx, acc.lo + h.lo_plane * pl, r.top + h.lo_plane * pl, n, bwd, fwd);
+    // hi chunk -> its owner r+d; from r-d into bot
+    xfer(ctx, acc.hi + h.hi_plane * pl, r.bot + h.hi_plane * pl, n, fwd, bwd);
+  }
   VB_NCCL(ncclGroupEnd());
   ctx->comm_bytes[C_SCATTER_POINTS] += 2 * gp * sizeof(float);
-  ctx->comm_bytes[C_P2P_MSGS] += 2;
+  ctx->comm_bytes[C_P2P_MSGS] += 2 * chunks.size();
   return r;
 }
 
 void halo_reverse_finish(vreg_ctx ctx, const Slab& s, const RevHalo& r, float* out,
                          bool as_int) {
-  const size_t gp = size_t(r.G) * s.plane();
+  const size_t pl = s.plane();
   Timed t(ctx, T_SCATTER_BUF);
-  if (as_int && s.n3 % 4 == 0) {  // packed pairs
-    k_add_planes_i64<<<blocks_for(gp / 2, 256), 256, 0, ctx->stream>>>(
-        gp / 2, reinterpret_cast<const long long*>(r.top),
-        reinterpret_cast<long long*>(out + size_t(s.n1l - r.G) * s.plane()));
-    k_add_planes_i64<<<blocks_for(gp / 2, 256), 256, 0, ctx->stream>>>(
-        gp / 2, reinterpret_cast<const long long*>(r.bot), reinterpret_cast<long long*>(out));
+  // chunk d adds into my last c planes (top) and my first c planes (bot);
+  // chunks overlap when G > n1l, so the adds stay stream-ordered
+  for (const HaloChunk& h : halo_chunks(s.n1l, r.G)) {
+    const size_t n = size_t(h.c) * pl;
+    const float* top = r.top + h.lo_plane * pl;
+    const float* bot = r.bot + h.hi_plane * pl;
+    float* otop = out + size_t(s.n1l - h.c) * pl;
+    if (as_int && s.n3 % 4 == 0) {  // packed pairs
+      k_add_planes_i64<<<blocks_for(n / 2, 256), 256, 0, ctx->stream>>>(
+          n / 2, reinterpret_cast<const long long*>(top), reinterpret_cast<long long*>(otop));
+      k_add_planes_i64<<<blocks_for(n / 2, 256), 256, 0, ctx->stream>>>(
+          n / 2, reinterpret_cast<const long long*>(bot), reinterpret_cast<long long*>(out));
+    } else if (as_int) {
+      k_add_planes_int<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(
+          n, reinterpret_cast<const int*>(top), reinterpret_cast<int*>(otop));
+      k_add_planes_int<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(
+          n, reinterpret_cast<const int*>(bot), reinterpret_cast<int*>(out));
+    } else {
+      k_add_planes<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(n, top, otop);
+      k_add_planes<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(n, bot, out);
+    }
     count_launch(ctx, 2);
     check_launch();
-    return;
   }
-  if (as_int) {
-    k_add_planes_int<<<blocks_for(gp, 256), 256, 0, ctx->stream>>>(
-        gp, reinterpret_cast<const int*>(r.top),
-        reinterpret_cast<int*>(out + size_t(s.n1l - r.G) * s.plane()));
-    k_add_planes_int<<<blocks_for(gp, 256), 256, 0, ctx->stream>>>(
-        gp, reinterpret_cast<const int*>(r.bot), reinterpret_cast<int*>(out));
-    count_launch(ctx, 2);
-    check_launch();
-    return;
-  }
-  k_add_planes<<<blocks_for(gp, 256), 256, 0, ctx->stream>>>(
-      gp, r.top, out + size_t(s.n1l - r.G) * s.plane());
-  k_add_planes<<<blocks_for(gp, 256), 256, 0, ctx->stream>>>(gp, r.bot, out);
-  count_launch(ctx, 2);
-  check_launch();
 }
 
 void halo_reverse_add(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, float* out,
@@ -233,8 +272,8 @@ void halo_reverse_add(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, float* o
 int sl_ghost_width(vreg_ctx ctx, const Slab& s, const float* disp1, int degree) {
   const double m = reduce(ctx, s, 1, disp1, disp1, true);
   const int G = int(std::floor(m)) + (degree == 3 ? 3 : 2);
-  require(G <= s.n1l, VREG_ECONFIG,
-          "departure points beyond the neighbouring slab (displacement > slab width)");
+  // wider than the slab: multi-rank (wide) halos, see halo_chunks
+  require(G <= 2 * s.n1, VREG_ECONFIG, "displacement exceeds twice the domain");
   return G;
 }
 
@@ -297,3 +336,16 @@ void dist_fft_inverse(vreg_ctx ctx, const Slab& s, int ncomp, float2* F, float* 
 }
 
 }  // namespace vb
+
+extern "C" int vreg_halo_chunks(int n1l, int G, int cap, int* d, int* c, long long* lo,
+                                long long* hi) {
+  if (n1l < 1 || G < 1 || cap < 0) return -1;
+  const auto v = vb::halo_chunks(n1l, G);
+  for (size_t i = 0; i < v.size() && int(i) < cap; ++i) {
+    d[i] = v[i].d;
+    c[i] = v[i].c;
+    lo[i] = (long long)v[i].lo_plane;
+    hi[i] = (long long)v[i].hi_plane;
+  }
+  return int(v.size());
+}

@@ -1302,8 +1302,7 @@ int sl_characteristics(vreg_ctx ctx, const Slab& s, const float* v3, int degree,
     // ghost width from the midpoint displacement bound dt max|v1| / h1
     const double vmax1 = reduce(ctx, s, 1, v3, v3, true);
     int G = int(std::floor(dt * vmax1 / s.h(0))) + (degree == 3 ? 3 : 2);
-    require(G <= s.n1l, VREG_ECONFIG,
-            "displacement exceeds the slab width (halo would span several ranks)");
+    require(G <= 2 * s.n1, VREG_ECONFIG, "displacement exceeds twice the domain");
     g1 = halo_exchange(ctx, s, v3, G, "chars_g1", T_INTERP_COMM, C_GHOST_INTERP);
     g2 = halo_exchange(ctx, s, v3 + N, G, "chars_g2", T_INTERP_COMM, C_GHOST_INTERP);
     g3 = halo_exchange(ctx, s, v3 + 2 * N, G, "chars_g3", T_INTERP_COMM, C_GHOST_INTERP);

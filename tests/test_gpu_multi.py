@@ -31,3 +31,20 @@ def test_slab_decomposed_matches_single_gpu(nproc, p2p):
     res = json.loads(lines[-1])
     assert res["ok"], res
     assert res["J_rel"] == 0.0 and res["grad_rel"] == 0.0  # bitwise p-independent
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_wide_halos_match_single_gpu(nproc):
+    """Ghost width beyond the slab width (nt=1, 8 x v_syn on 32^3): the
+    multi-rank halo chunks (csrc/dist.cu halo_chunks) against 1 GPU."""
+    if torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    env = dict(os.environ, NCCL_DEBUG="WARN")
+    r = subprocess.run(["timeout", "600", sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
+                        f"--master-port={29700 + nproc}", os.path.join(ROOT, "tools", "mgpu_check.py"),
+                        "32", "wide"], capture_output=True, text=True, timeout=900, env=env)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-2000:]
+    res = json.loads(lines[-1])
+    assert res["ok"], res

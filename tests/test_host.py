@@ -157,3 +157,62 @@ def test_volume_file_roundtrip_and_errors(tmp_path):
     with pytest.raises(VregError) as e:
         load_volume(tmp_path / "missing.vrg")
     assert e.value.kind == "io_error"
+
+
+def _halo_plan(n1l, G):
+    from paper_2008_12820_b200 import _lib
+    cap = 256
+    d, c = (C.c_int * cap)(), (C.c_int * cap)()
+    lo, hi = (C.c_longlong * cap)(), (C.c_longlong * cap)()
+    n = _lib.lib().vreg_halo_chunks(n1l, G, cap, d, c, lo, hi)
+    assert 0 < n <= cap
+    return [(d[i], c[i], lo[i], hi[i]) for i in range(n)]
+
+
+@pytest.mark.parametrize("p,n1l,G", [(2, 16, 3), (2, 16, 16), (2, 16, 23), (4, 8, 23),
+                                     (3, 5, 14), (1, 8, 3), (4, 8, 40), (8, 2, 7)])
+def test_wide_halo_plan(p, n1l, G):
+    """Halo chunks of csrc/dist.cu (vreg_halo_chunks) for ghost widths up to
+    and beyond the slab width: every rank's lo/hi ghosts hold the periodic
+    neighbour planes, the reverse exchange folds ghost accumulators onto
+    their owners, and the send/recv issue order (dist.cu halo_exchange /
+    halo_reverse_send) matches per peer pair, as NCCL's in-order matching
+    of same-peer messages needs."""
+    chunks = _halo_plan(n1l, G)
+    assert sum(c for _, c, _, _ in chunks) == G
+    n1 = p * n1l
+    for r in range(p):
+        lo, hi = np.full(G, -1), np.full(G, -1)
+        for d, c, l, h in chunks:
+            a, b = (r - d) % p, (r + d) % p
+            lo[l:l + c] = np.arange(a * n1l + n1l - c, a * n1l + n1l)
+            hi[h:h + c] = np.arange(b * n1l, b * n1l + c)
+        assert np.array_equal(lo, (r * n1l - G + np.arange(G)) % n1)
+        assert np.array_equal(hi, (r * n1l + n1l + np.arange(G)) % n1)
+    # reverse fold: extended accumulators [-G, n1l + G) per rank -> owners
+    rng = np.random.default_rng(G)
+    ext = rng.standard_normal((p, n1l + 2 * G))
+    expect = np.zeros(n1)
+    for r in range(p):
+        np.add.at(expect, (r * n1l - G + np.arange(n1l + 2 * G)) % n1, ext[r])
+    got = ext[:, G:G + n1l].copy()
+    for r in range(p):
+        for d, c, l, h in chunks:
+            got[(r - d) % p, n1l - c:] += ext[r, l:l + c]          # lo chunk -> owner r-d
+            got[(r + d) % p, :c] += ext[r, G + n1l + h:G + n1l + h + c]  # hi chunk -> owner r+d
+    assert np.allclose(got.reshape(-1), expect)
+    # issue order, forward and reverse (self transfers are local copies)
+    for rev in (False, True):
+        sends = {(a, b): [] for a in range(p) for b in range(p)}
+        recvs = {(a, b): [] for a in range(p) for b in range(p)}
+        for r in range(p):
+            for d, c, _, _ in chunks:
+                f, b = (r + d) % p, (r - d) % p
+                pairs = [(b, f, "lo"), (f, b, "hi")] if rev else [(f, b, "lo"), (b, f, "hi")]
+                for to, frm, tag in pairs:
+                    if to == r:
+                        continue
+                    sends[(r, to)].append((tag, d, c))
+                    recvs[(frm, r)].append((tag, d, c))
+        for k in sends:
+            assert sends[k] == recvs[k], (rev, k)

@@ -71,6 +71,55 @@ def run(ctx, dims, beta):
     return out
 
 
+def run_wide(ctx, dims, beta, scale=8.0):
+    """Large displacements (nt=1, scale x v_syn): ghost widths beyond the slab
+    width, i.e. multi-rank ("wide") halos, csrc/dist.cu halo_chunks."""
+    cfg = Config(continuation=False, beta_target=beta, precond="inva", nt=1)
+    s = Solver(ctx, dims, cfg)
+    s.syn_images()
+    g = s.grid
+    v = (scale * ctx.syn_velocity(g)).contiguous()
+    s.linearize(v, beta)
+    J = s.objective()
+    grad = s.gradient()
+    vt = (-grad).contiguous()
+    H = s.matvec(vt)
+    ctx.set_deterministic(True)
+    Hd = s.matvec(vt)
+    ctx.set_deterministic(False)
+    _, flags = ctx.characteristics(g, v, 3)
+    out = {"J": J, "grad": ctx.to_global(g, grad), "H": ctx.to_global(g, H),
+           "Hdet": ctx.to_global(g, Hd), "G": int(flags) >> 8}
+    s.close()
+    return out
+
+
+def wide_main(n):
+    ctx, rank, world, local = init_from_env()
+    dims = (n, n, n)
+    beta = 1e-3
+    d = run_wide(ctx, dims, beta)
+    ok = True
+    if rank == 0:
+        single = Context(local)
+        r = run_wide(single, dims, beta)
+        res = {"world": world, "grid": dims, "ghost_width": d["G"] - 1, "slab_width": n // world,
+               "J_rel": abs(d["J"]["total"] / r["J"]["total"] - 1)}
+        for k in ("grad", "H", "Hdet"):
+            res[f"{k}_rel"] = rel(d[k], r[k].astype(np.float64))
+        ok = (res["ghost_width"] > res["slab_width"] and res["J_rel"] < 1e-6 and
+              res["grad_rel"] < 1e-5 and res["H_rel"] < 1e-5 and res["Hdet_rel"] == 0.0)
+        res["ok"] = ok
+        print(json.dumps(res), flush=True)
+        single.close()
+    flag = torch.tensor([1 if ok else 0], device="cuda")
+    dist.broadcast(flag, 0) if world > 1 else None
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    sys.exit(0 if int(flag.item()) else 1)
+
+
 def VregGridC(g):
     from paper_2008_12820_b200 import VregGrid
     return VregGrid(g.n1 // 2, g.n2 // 2, g.n3 // 2, g.nt)
@@ -82,6 +131,8 @@ def rel(a, b):
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+    if len(sys.argv) > 2 and sys.argv[2] == "wide":
+        return wide_main(n)
     ctx, rank, world, local = init_from_env()
     dims = (n, n // 2 * 2 if n >= 16 else n, n)
     beta = 1e-3
