@@ -368,6 +368,30 @@ def run_ours(args):
             "gn_iters": rep["total_gn"], "pcg_iters": rep["total_pcg"], "levels": rep["levels"],
             "mism_rel": rep["mism_rel"], "final_g_rel": rep["final_g_rel"],
             "phases_s": {k: rep[f"t_{k}"] for k in ("pc", "obj", "grad", "hess")}}
+    # ---- trilinear matvec at the same linearisation (the paper's scaling runs
+    # used linear interpolation; SURVEY §8d reports both)
+    if deg == 3 and not args.no_linear:
+        lin = Solver(ctx, dims, Config(continuation=False, beta_target=BETA, interp_degree=1,
+                                       nt=NT))
+        lin.syn_images()
+        v1 = (0.5 * ctx.syn_velocity(g)).contiguous()
+        lin.linearize(v1, BETA)
+        vt1 = (-lin.gradient()).contiguous()
+        del v1
+        out1 = torch.empty_like(vt1)
+        for _ in range(3):
+            lin.matvec(vt1, out1)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            lin.matvec(vt1, out1)
+        ev1.record(stream)
+        barrier()
+        lms = max_over_ranks(ev0.elapsed_time(ev1))
+        extra["linear"] = {"interp_degree": 1, "value": Nvox * args.steps / (lms * 1e-3) / 1e6,
+                           "unit": UNIT, "ms_per_step": lms / args.steps}
+        lin.close()
+        del vt1, out1
     nbytes = vt.numel() * 4
 
     if rank == 0:
@@ -477,6 +501,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=256, help="per-GPU cube edge (weak scaling family)")
     ap.add_argument("--degree", type=int, default=3)
+    ap.add_argument("--no-linear", action="store_true", help="skip the trilinear matvec line")
     ap.add_argument("--grid", default="", help="explicit global grid n1,n2,n3 (overrides --size)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-registration", action="store_true",

@@ -5,7 +5,7 @@ python -m pytest tests -x -q -m gpu 2>&1 | tail -3 > gpurun_out/gpu_tests.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 python bench.py --steps 20 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-B="python bench.py --steps 2 --warmup 3 --no-cpu --no-registration"
+B="python bench.py --steps 2 --warmup 3 --no-cpu --no-registration --no-linear"
 $B > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_l.log 2>&1
 K="--set full --clock-control none --import-source on --kernel-name-base demangled"
