@@ -220,6 +220,10 @@ class Timed {
 
 inline void count_launch(vreg_ctx ctx, uint64_t n = 1) { ctx->launches += n; }
 
+// Opt a kernel in to `bytes` of dynamic shared memory on the current device
+// (function attributes are per device: once per (device, kernel), thread-safe).
+void smem_optin(const void* kernel, int bytes);
+
 inline void check_launch() { VB_CUDA(cudaGetLastError()); }
 
 inline unsigned blocks_for(size_t n, unsigned threads, unsigned cap = 148u * 32u) {

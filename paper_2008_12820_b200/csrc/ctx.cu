@@ -6,11 +6,24 @@
 #include <cstdio>
 #include <cstring>
 #include <iterator>
+#include <map>
 #include <mutex>
 
 #include "common.cuh"
 
 namespace vb {
+
+void smem_optin(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  VB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{dev, kernel}];
+  if (have >= bytes) return;
+  VB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
+}
 
 namespace {
 thread_local std::string g_last_error;

@@ -830,13 +830,7 @@ constexpr size_t kTileSmem = kTileCap * sizeof(float);
 // Opt a tile kernel in to kTileSmem of dynamic shared memory (once).
 template <class Kern>
 inline Kern tile_kernel(Kern k) {
-  static std::set<const void*> done;  // per kernel (same-signature kernels share Kern)
-  const void* key = reinterpret_cast<const void*>(k);
-  if (!done.count(key)) {
-    VB_CUDA(cudaFuncSetAttribute(key, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(kTileSmem)));
-    done.insert(key);
-  }
+  smem_optin(reinterpret_cast<const void*>(k), int(kTileSmem));
   return k;
 }
 

@@ -271,12 +271,7 @@ void launch_axis(vreg_ctx ctx, const AxisGeom& s, int n, const float* v3, float*
   case NN: {                                                                               \
     const size_t smem = size_t(AxisShape<NN>::NP) *                                        \
                         ((NN / AxisShape<NN>::T1) * (AxisShape<NN>::T1 + 1) + 1) * sizeof(float2); \
-    static const bool attr = [&] {                                                         \
-      VB_CUDA(cudaFuncSetAttribute(k_axis_d2<NN, AX>,                                      \
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); \
-      return true;                                                                         \
-    }();                                                                                   \
-    (void)attr;                                                                            \
+    smem_optin(reinterpret_cast<const void*>(k_axis_d2<NN, AX>), int(smem));           \
     k_axis_d2<NN, AX><<<grid, AX_THREADS, smem, ctx->stream>>>(s.n1l, s.n2, s.n3, tiles, v3, \
                                                                out3, tw, coef, accumulate, \
                                                                bias_sums, bias_scale);     \
