@@ -208,3 +208,27 @@ def test_matvec_on_irregular_grids(ctx, shape):
     if p is not None:
         ref_p, _ = r.precond("2linvh0", -g, 0.5)
         assert rel(host(p), ref_p) < 1e-4
+
+
+def test_probe_goldens_256(ctx):
+    """SURVEY §8c probe goldens at 256^3 (fp64 reference run, BASELINE
+    configs[1] linearisation: SYN, nt=4, cubic, beta=1e-3, v = 0.5 v_syn,
+    vt = -g): J, mismatch, ||g||, ||H vt||, <vt, H vt>."""
+    n = 256
+    s = Solver(ctx, n, Config(continuation=False, beta_target=BETA))
+    s.syn_images()
+    s.linearize((0.5 * ctx.syn_velocity(s.grid)).contiguous(), BETA)
+    J = s.objective()
+    g = s.gradient()
+    vt = (-g).contiguous()
+    H = s.matvec(vt)
+    h3 = (2 * np.pi / n) ** 3
+    gn = float(torch.sqrt((g.double() ** 2).sum() * h3))
+    hn = float(torch.sqrt((H.double() ** 2).sum() * h3))
+    vh = float((vt.double() * H.double()).sum() * h3)
+    golden = {"J": 3.4420142603e-1, "mismatch": 3.1513304165e-1, "g": 3.7035705258e-1,
+              "H": 9.8485730595e-2, "vH": 3.5359314462e-2}
+    got = {"J": J["total"], "mismatch": J["mismatch"], "g": gn, "H": hn, "vH": vh}
+    for k in golden:
+        assert abs(got[k] / golden[k] - 1) < 1e-4, (k, got[k], golden[k])
+    s.close()
