@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -288,6 +289,15 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = Nvox * args.steps / (ms * 1e-3) / 1e6
+    # the timed matvec's result against the SURVEY §8c probe golden ||H vt||
+    # (fp64 reference run, 256^3 SYN linearisation)
+    hh = torch.tensor([float((out.double() ** 2).sum())], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(hh)
+    h_norm = float(torch.sqrt(hh * (2 * math.pi) ** 3 / Nvox))
+    golden = {(256, 256, 256): 9.8485730595e-2, (64, 64, 64): 9.8356971587e-2}.get(tuple(dims))
+    check = {"H_norm": h_norm, "golden": golden,
+             "rel": abs(h_norm / golden - 1) if golden and deg == 3 else None}
 
     # ---- e2e: the public API with HOST buffers, copies inside the timed region.
     # vreg_solver_matvec_host_async pipelines call k's upload, call k-1's
@@ -473,6 +483,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": nbytes, "ms_per_step": ms_e2e / args.steps,
                     "api": "vreg_solver_matvec_host_async (pinned host buffers, 2 slots)",
                     "rel_diff_vs_blocking_call": e2e_diff},
+            "result_check": check,
             "gpu_launches": launches,
             "sl_tiles": dict(zip(("built", "over_smem_budget"), ctx.tile_stats())),
             "clocks": clk.summary(),
