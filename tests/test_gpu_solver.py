@@ -232,3 +232,21 @@ def test_probe_goldens_256(ctx):
     for k in golden:
         assert abs(got[k] / golden[k] - 1) < 1e-4, (k, got[k], golden[k])
     s.close()
+
+
+@pytest.mark.parametrize("nt,degree", [(1, 3), (2, 3), (3, 1), (8, 3)])
+def test_matvec_time_steps(ctx, nt, degree):
+    """The fused matvec's time-step bookkeeping (w slot parity, u_t indexing,
+    nt+1 psi slices, trapezoid weights) for nt other than 4, both degrees."""
+    n = 32
+    m0, v, m1 = ref.syn(n, nt, degree)
+    cfg = Config(continuation=False, beta_target=BETA, nt=nt, interp_degree=degree)
+    s = Solver(ctx, n, cfg)
+    s.set_images(dev(m0), dev(m1))
+    s.linearize(dev(0.5 * v), BETA)
+    r = ref.Session(m0, m1, 0.5 * v, BETA, ref.Config(continuation=False, beta_target=BETA,
+                                                      nt=nt, interp_degree=degree))
+    g = r.gradient()
+    assert rel(host(s.gradient()), g) < 1e-5
+    assert rel(host(s.matvec(dev(-g))), r.matvec(-g)) < 1e-5
+    s.close()
