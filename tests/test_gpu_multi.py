@@ -48,3 +48,20 @@ def test_wide_halos_match_single_gpu(nproc):
     assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-2000:]
     res = json.loads(lines[-1])
     assert res["ok"], res
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_irregular_grid_matches_single_gpu(nproc):
+    """48x40x36 (not powers of two): the regulariser's cuFFT slab path with
+    all-to-alls, partial tiles, the distributed two-level transfers."""
+    if torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    env = dict(os.environ, NCCL_DEBUG="WARN")
+    r = subprocess.run(["timeout", "600", sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
+                        f"--master-port={29720 + nproc}", os.path.join(ROOT, "tools", "mgpu_check.py"),
+                        "48,40,36"], capture_output=True, text=True, timeout=900, env=env)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-2000:]
+    res = json.loads(lines[-1])
+    assert res["ok"], res

@@ -130,11 +130,15 @@ def rel(a, b):
 
 
 def main():
-    n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+    arg = sys.argv[1] if len(sys.argv) > 1 else "64"
     if len(sys.argv) > 2 and sys.argv[2] == "wide":
-        return wide_main(n)
+        return wide_main(int(arg))
     ctx, rank, world, local = init_from_env()
-    dims = (n, n // 2 * 2 if n >= 16 else n, n)
+    if "," in arg:  # explicit grid, e.g. 48,40,36 (non power-of-two: cuFFT slab paths)
+        dims = tuple(int(x) for x in arg.split(","))
+    else:
+        n = int(arg)
+        dims = (n, n // 2 * 2 if n >= 16 else n, n)
     beta = 1e-3
     dist_out = run(ctx, dims, beta)
     ok = True
