@@ -354,7 +354,9 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_gather_tile(
       box_rows<DIST>(g, src, b, rows);
       __syncthreads();
     }
+#ifndef VB_DIAG_NOBOX  // timing diagnostics only (wrong results): no box staging
     load_box(g, src, b, fbox, rows);
+#endif
   }
   // prefetch the points' displacements (and, MODE 2, the precomputed
   // u = vt . grad m_{t+1} passed in qf) while the box streams in
@@ -376,7 +378,11 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_gather_tile(
     float G;
     BoxStencil<DEG> bs;
     if (fits && bs.build(b, i, j, k, d1[it], d2[it], d3[it]))
+#ifndef VB_DIAG_NOTAPS  // timing diagnostics only (wrong results): no tap contraction
       G = bs.gather(b, fbox);
+#else
+      G = bs.w1[0] + bs.w2[1] + bs.w3[2] + float(bs.base);
+#endif
     else
       G = point_gather<DEG, DIST>(g, src, i, j, k, d1[it], d2[it], d3[it]);
     if constexpr (MODE == 0) {
