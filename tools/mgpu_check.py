@@ -40,9 +40,16 @@ def run(ctx, dims, beta):
     ctx.set_deterministic(False)
     P, _ = s.precond("inva", vt, 0.5)
     m0, m1 = s.images()
+    # optimize-then-discretize (SL incremental adjoint) Hessian, optim.hpp:125-128
+    s_sl = Solver(ctx, dims, Config(continuation=False, beta_target=beta, precond="inva",
+                                    hessian_adjoint=1))
+    s_sl.syn_images()
+    s_sl.linearize(v, beta)
+    H_sl = ctx.to_global(g, s_sl.matvec(vt))
+    s_sl.close()
     out = {"J": J, "grad": ctx.to_global(g, grad), "H": ctx.to_global(g, H),
            "Hdet": ctx.to_global(g, Hd),
-           "P": ctx.to_global(g, P), "m1": ctx.to_global(g, m1)}
+           "P": ctx.to_global(g, P), "m1": ctx.to_global(g, m1), "H_sl": H_sl}
     s.close()
     cfg2 = Config(continuation=False, beta_target=beta, precond="inva", fixed_gn=2, fixed_pcg=3)
     s2 = Solver(ctx, dims, cfg2)
@@ -148,15 +155,15 @@ def main():
         ref = run(single, dims, beta)
         res["J_rel"] = abs(dist_out["J"]["total"] / ref["J"]["total"] - 1)
         res["mismatch_rel"] = abs(dist_out["J"]["mismatch"] / ref["J"]["mismatch"] - 1)
-        for k in ("m1", "grad", "H", "Hdet", "P", "v", "regop", "restrict", "high_pass", "P2",
-                  "v2l"):
+        for k in ("m1", "grad", "H", "Hdet", "H_sl", "P", "v", "regop", "restrict", "high_pass",
+                  "P2", "v2l"):
             res[f"{k}_rel"] = rel(dist_out[k], ref[k].astype(np.float64))
         res["solve_mismatch_rel"] = abs(dist_out["solve"]["final_mismatch"] /
                                         ref["solve"]["final_mismatch"] - 1)
         res["solve2l_mismatch_rel"] = abs(dist_out["solve2l"]["final_mismatch"] /
                                           ref["solve2l"]["final_mismatch"] - 1)
         ok = (res["m1_rel"] < 1e-6 and res["J_rel"] < 1e-6 and res["grad_rel"] < 1e-5 and
-              res["H_rel"] < 1e-5 and res["P_rel"] < 1e-5 and res["v_rel"] < 1e-4 and
+              res["H_rel"] < 1e-5 and res["H_sl_rel"] < 1e-5 and res["P_rel"] < 1e-5 and res["v_rel"] < 1e-4 and
               res["solve_mismatch_rel"] < 1e-4 and res["restrict_rel"] < 1e-5 and
               res["high_pass_rel"] < 1e-5 and res["P2_rel"] < 1e-4 and res["v2l_rel"] < 1e-4 and
               res["solve2l_mismatch_rel"] < 1e-4 and res["regop_rel"] == 0.0 and
