@@ -40,14 +40,14 @@ __device__ __forceinline__ void fixed_add(int* p, int v, bool packed) {
 }
 __device__ __forceinline__ bool fixed_packed(const Geo& g) { return (g.n3 & 3) == 0; }
 
+// base = q + floor(d), s = d - floor(d) in [0, 1]. s rounds to 1 only for
+// tiny negative d; the cubic / linear weights at s = 1 are exactly
+// (0, 0, 1, 0) / (0, 1), i.e. the node value, so no snap branch is needed
+// (and k_tile_boxes' reach, floor(d), stays the same).
 __device__ __forceinline__ void split_axis(float d, int q, int& base, float& s) {
   const float fd = floorf(d);
-  s = d - fd;  // exact in fp32
+  s = d - fd;
   base = q + int(fd);
-  if (s >= 1.0f) {  // unreachable for finite d, kept as the snap guard
-    s = 0.0f;
-    ++base;
-  }
 }
 
 __device__ __forceinline__ int wrap_mod(int b, int n) {
