@@ -63,11 +63,14 @@ __device__ __forceinline__ int wrap1(int b, int n) {
 template <int DEG>
 __device__ __forceinline__ void lagrange_weights(float s, float* w) {
   if constexpr (DEG == 3) {
-    const float sm = s - 1.0f, sp = s + 1.0f, s2 = s - 2.0f;
-    w[0] = -s * sm * s2 * (1.0f / 6.0f);
-    w[1] = sp * sm * s2 * 0.5f;
-    w[2] = -sp * s * s2 * 0.5f;
-    w[3] = sp * s * sm * (1.0f / 6.0f);
+    // factored: q = -s (1-s) / 6, r = (s+1)(2-s) / 2; w = (q (2-s), r (1-s), r s, q (s+1))
+    const float ms = 1.0f - s, sp = s + 1.0f, ns2 = 2.0f - s;
+    const float q = __fmul_rn(__fmul_rn(s, ms), -1.0f / 6.0f);
+    const float r = __fmul_rn(__fmul_rn(sp, ns2), 0.5f);
+    w[0] = __fmul_rn(q, ns2);
+    w[1] = __fmul_rn(r, ms);
+    w[2] = __fmul_rn(r, s);
+    w[3] = __fmul_rn(q, sp);
   } else {
     w[0] = 1.0f - s;
     w[1] = s;
