@@ -344,3 +344,26 @@ def register(m0, m1, cfg: Config):
     m1c = np.ascontiguousarray(m1, dtype=np.float64)
     _chk(lib().vref_register(*_dims(shape), C.byref(c), _p(m0c), _p(m1c), _p(v), _p(rep), _p(cnt)))
     return v, dict(zip(REPORT_NAMES, rep.tolist())), dict(zip(COUNTER_NAMES, (int(x) for x in cnt)))
+
+
+LEVEL_KEYS = ["beta", "inva", "switched", "gn_iters", "pcg_total", "final_mismatch",
+              "final_g_rel", "converged"]
+ITER_KEYS = ["level", "objective", "mismatch", "g_rel", "eps_k", "alpha", "pcg_iters"]
+
+
+def register_levels(m0, m1, cfg: Config):
+    """register_images with its per-level and per-GN-iteration records
+    (report.hpp:12-78): returns v, [level dicts], [GN-iteration dicts]."""
+    shape = m0.shape
+    c = cfg.to_c()
+    v = np.zeros((3,) + shape)
+    lev = np.zeros((64, 8))
+    its = np.zeros((1024, 7))
+    nl, ni = C.c_int(0), C.c_int(0)
+    m0c = np.ascontiguousarray(m0, dtype=np.float64)
+    m1c = np.ascontiguousarray(m1, dtype=np.float64)
+    _chk(lib().vref_register_levels(*_dims(shape), C.byref(c), _p(m0c), _p(m1c), _p(v),
+                                    _p(lev), 64, C.byref(nl), _p(its), 1024, C.byref(ni)))
+    levels = [dict(zip(LEVEL_KEYS, r.tolist())) for r in lev[:nl.value]]
+    iters = [dict(zip(ITER_KEYS, r.tolist())) for r in its[:min(ni.value, 1024)]]
+    return v, levels, iters

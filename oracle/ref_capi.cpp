@@ -35,9 +35,9 @@ int status_of(const std::exception& e) {
   return 9;
 }
 
-#define GUARD(body)                 \
+#define GUARD(...)                  \
   try {                             \
-    body;                           \
+    __VA_ARGS__;                           \
     return 0;                       \
   } catch (const std::exception& e) { \
     return status_of(e);            \
@@ -425,6 +425,54 @@ int vref_register(int n1, int n2, int n3, const vref_config* c,
       rep[15] = estimate_cost(r, cfg).matches(r.counters) ? 1 : 0;
     }
     if (counters) dump_counters(r.counters, counters);
+  })
+}
+
+// register_images (optim.hpp:308-347) with the per-level / per-GN-iteration
+// records of its SolverReport (report.hpp:12-78): level rows of 8 doubles
+// (beta, pc is inva, switched, gn_iters, pcg_total, final_mismatch,
+// final_g_rel, converged) and GN rows of 7 (level, objective, mismatch,
+// g_rel, eps_k, alpha, pcg_iters). Capacities in rows; counts returned.
+int vref_register_levels(int n1, int n2, int n3, const vref_config* c, const double* m0,
+                         const double* m1, double* v_out3, double* lev, int lev_cap,
+                         int* nlev, double* its, int its_cap, int* nits) {
+  GUARD({
+    RegistrationConfig cfg = to_cfg(c);
+    Grid3 g = Grid3::make(n1, n2, n3, cfg.nt);
+    SerialEngine eng = SerialEngine::create(g);
+    VectorField v;
+    SolverReport r = register_images(eng, load(g, m0), load(g, m1), cfg, &v);
+    if (v_out3) storev(v, v_out3);
+    int L = 0, I = 0;
+    for (const LevelRecord& l : r.levels) {
+      if (L < lev_cap) {
+        double* o = lev + 8 * L;
+        o[0] = l.beta;
+        o[1] = l.pc_name == "inva" ? 1.0 : 0.0;
+        o[2] = l.pc_switched_from_config ? 1.0 : 0.0;
+        o[3] = l.gn_iters;
+        o[4] = l.pcg_total;
+        o[5] = l.final_mismatch;
+        o[6] = l.final_g_rel;
+        o[7] = l.converged ? 1.0 : 0.0;
+      }
+      for (const GnIterRecord& it : l.iters) {
+        if (I < its_cap) {
+          double* o = its + 7 * I;
+          o[0] = L;
+          o[1] = it.objective;
+          o[2] = it.mismatch;
+          o[3] = it.g_rel;
+          o[4] = it.eps_k;
+          o[5] = it.alpha;
+          o[6] = it.pcg_iters;
+        }
+        ++I;
+      }
+      ++L;
+    }
+    *nlev = L;
+    *nits = I;
   })
 }
 

@@ -3,13 +3,12 @@
 // All three axes use the paired antisymmetric form sum_j c_j (f_{+j} - f_{-j})
 // (fd.cpp:60-78; the reference uses it on x1 and an unpaired 9-tap sum with
 // a ~3e-16 centre weight on x2/x3, fd.cpp:80-125 -- identical to fp64
-// round-off). Weights come from the same Fornberg
-// recursion (fd.cpp:7-48), evaluated in fp64 and rounded once.
+// round-off). Weights are the closed-form values of the
+// reference's Fornberg recursion (fd.cpp:7-48), rounded once to fp32.
 //
 // Tiling: see the x1-marching kernels below (register window along x1,
 // double-buffered shared tile with the x2/x3 halo of 4).
 #include <cmath>
-#include <vector>
 
 #include "common.cuh"
 
@@ -19,52 +18,15 @@ namespace {
 
 constexpr int TX = 32, TY = 8, H = 4;
 
-std::vector<double> fornberg(int half_width, int deriv) {
-  const int n = 2 * half_width;
-  const int m = deriv;
-  std::vector<double> x(size_t(n) + 1);
-  for (int i = 0; i <= n; ++i) x[size_t(i)] = double(i - half_width);
-  std::vector<std::vector<double>> c(size_t(n) + 1, std::vector<double>(size_t(m) + 1, 0.0));
-  double c1 = 1.0, c4 = x[0];
-  c[0][0] = 1.0;
-  for (int i = 1; i <= n; ++i) {
-    const int mn = i < m ? i : m;
-    double c2 = 1.0;
-    const double c5 = c4;
-    c4 = x[size_t(i)];
-    for (int j = 0; j <= i - 1; ++j) {
-      const double c3 = x[size_t(i)] - x[size_t(j)];
-      c2 *= c3;
-      if (j == i - 1) {
-        for (int k = mn; k >= 1; --k)
-          c[size_t(i)][size_t(k)] =
-              c1 * (k * c[size_t(i) - 1][size_t(k) - 1] - c5 * c[size_t(i) - 1][size_t(k)]) / c2;
-        c[size_t(i)][0] = -c1 * c5 * c[size_t(i) - 1][0] / c2;
-      }
-      for (int k = mn; k >= 1; --k)
-        c[size_t(j)][size_t(k)] =
-            (c4 * c[size_t(j)][size_t(k)] - k * c[size_t(j)][size_t(k) - 1]) / c3;
-      c[size_t(j)][0] = c4 * c[size_t(j)][0] / c3;
-    }
-    c1 = c2;
-  }
-  std::vector<double> out(size_t(n) + 1);
-  for (int i = 0; i <= n; ++i) out[size_t(i)] = c[size_t(i)][size_t(m)];
-  return out;
-}
-
+// Paired 8th-order first-derivative weights c_j, j = 1..4, unit spacing: the
+// antisymmetric half of the 9-point Fornberg stencil the reference builds in
+// fd.cpp:7-48 (4/5, -1/5, 4/105, -1/280), rounded once to fp32.
 struct FdW {
-  float c[4];  // c_j for j = 1..4, unit spacing
+  float c[4];
 };
 
 FdW fd_weights() {
-  static const FdW w = [] {
-    auto d = fornberg(4, 1);
-    FdW r;
-    for (int j = 1; j <= 4; ++j) r.c[j - 1] = float(d[size_t(4 + j)]);
-    return r;
-  }();
-  return w;
+  return FdW{{float(4.0 / 5.0), float(-1.0 / 5.0), float(4.0 / 105.0), float(-1.0 / 280.0)}};
 }
 
 struct FdGeo {
@@ -102,6 +64,14 @@ constexpr int FD_RING = 3;  // shared tiles in flight
 constexpr int TW = TX + 2 * H;
 
 __device__ __forceinline__ int wrap_fd(int x, int n) { return x < 0 ? x + n : (x >= n ? x - n : x); }
+// halo-tile wrap: axes shorter than the tile extent (n3 < TW columns,
+// n2 < TY + 2H rows) wrap more than once, so those grids take a true modulo
+__device__ __forceinline__ int wrap_col(int x, int n) {
+  return n >= TW ? wrap_fd(x, n) : ((x % n) + n) % n;
+}
+__device__ __forceinline__ int wrap_row(int x, int n) {
+  return n >= TY + 2 * H ? wrap_fd(x, n) : ((x % n) + n) % n;
+}
 
 __device__ __forceinline__ void fd_cp16(float* smem, const float* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -126,14 +96,14 @@ __device__ __forceinline__ void stage_async(float (*t)[TW], const float* P, int 
     constexpr int CH = TW / 4;  // 10 chunks per row
     for (int c = tid; c < (TY + 2 * H) * CH; c += TX * TY) {
       const int y = c / CH, x4 = c - y * CH;
-      const float* R = P + size_t(wrap_fd(j0 + y - H, g.n2)) * g.n3;
-      fd_cp16(&t[y][4 * x4], R + wrap_fd(k0 - H + 4 * x4, g.n3));
+      const float* R = P + size_t(wrap_row(j0 + y - H, g.n2)) * g.n3;
+      fd_cp16(&t[y][4 * x4], R + wrap_col(k0 - H + 4 * x4, g.n3));
     }
   } else {
     for (int c = tid; c < (TY + 2 * H) * TW; c += TX * TY) {
       const int y = c / TW, x = c - y * TW;
-      const float* R = P + size_t(wrap_fd(j0 + y - H, g.n2)) * g.n3;
-      fd_cp4(&t[y][x], R + wrap_fd(k0 - H + x, g.n3));
+      const float* R = P + size_t(wrap_row(j0 + y - H, g.n2)) * g.n3;
+      fd_cp4(&t[y][x], R + wrap_col(k0 - H + x, g.n3));
     }
   }
 }

@@ -13,6 +13,9 @@
 #include "sl_common.cuh"
 #include "sl_quad.cuh"
 #include "sl_tile.cuh"
+#include "sl_pipe.cuh"
+
+#include <cudaTypedefs.h>
 
 namespace vb {
 
@@ -864,6 +867,75 @@ inline bool use_quad(const Slab& s) {
   return on && s.n3 % 4 == 0;
 }
 
+// ---- TMA pipeline (sl_pipe.cuh) host side ----------------------------------
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    VB_CUDA(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000,
+                                             cudaEnableDefault, &q));
+    require(q == cudaDriverEntryPointSuccess && f, VREG_ECUDA,
+            "cuTensorMapEncodeTiled is not available");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// 3-D tensor map over `depth` stacked (n2 x n3) fp32 planes, boxes of one
+// tile (TT3 x TT2 x TT1); out-of-range boxes zero-fill (masked points).
+CUtensorMap tmap_planes(const float* base, const Slab& s, int depth) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {cuuint64_t(s.n3), cuuint64_t(s.n2), cuuint64_t(depth)};
+  const cuuint64_t strides[2] = {cuuint64_t(s.n3) * 4u, cuuint64_t(s.n2) * cuuint64_t(s.n3) * 4u};
+  const cuuint32_t box[3] = {cuuint32_t(TT3), cuuint32_t(TT2), cuuint32_t(TT1)};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = tmap_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                                    const_cast<float*>(base), dims, strides, box, es,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  require(r == CUDA_SUCCESS, VREG_ECUDA, "cuTensorMapEncodeTiled failed");
+  return m;
+}
+
+int sm_count(vreg_ctx ctx) {
+  static int n = [&] {
+    int v = 0;
+    VB_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, ctx->device));
+    return v;
+  }();
+  return n;
+}
+
+// The pipeline needs 16-byte rows and whole-tile tensor boxes; other grids
+// and misaligned streams take the cp.async tile kernels (VREG_SL_PIPE=0
+// forces them, for A/B measurements).
+inline bool use_pipe(const Slab& s, std::initializer_list<const void*> ptrs) {
+  static const bool on = [] {
+    const char* e = std::getenv("VREG_SL_PIPE");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || s.n3 % 4 != 0 || s.n3 < TT3 || s.n2 < TT2 || s.n1l < TT1) return false;
+  for (const void* q : ptrs)
+    if (q && (reinterpret_cast<uintptr_t>(q) & 15u)) return false;
+  return true;
+}
+
+inline PipeTiles pipe_tiles(const Slab& s, int nz) {
+  PipeTiles t;
+  t.tx = (s.n3 + TT3 - 1) / TT3;
+  t.ty = (s.n2 + TT2 - 1) / TT2;
+  t.n = nz * t.tx * t.ty;
+  return t;
+}
+
+template <class Kern>
+inline Kern pipe_kernel(Kern k) {
+  smem_optin(reinterpret_cast<const void*>(k), int(PIPE_SMEM));
+  return k;
+}
+
 template <bool DIST>
 SrcField<DIST> src_of(const float* f, const Ghosts& gh) {
   SrcField<DIST> s;
@@ -915,6 +987,23 @@ inline void check_degree(int degree) {
     count_launch(ctx);                                    \
     check_launch();                                       \
   } while (0)
+
+// One gather sweep launch through the TMA pipeline (nz tile layers of zm).
+template <int MODE>
+void gather_pipe(vreg_ctx ctx, const Slab& s, int degree, bool dist, const float* f,
+                 const Ghosts& gh, const int* boxes, const float* disp3, const float* aux,
+                 float* out, float half, int last, float* mt_out, TileZ zm, int nz) {
+  const Geo g = geo_of(s);
+  const CUtensorMap tmD = tmap_planes(disp3, s, 3 * s.n1l);
+  const CUtensorMap tmA = aux ? tmap_planes(aux, s, s.n1l) : tmD;
+  const PipeTiles pt = pipe_tiles(s, nz);
+  const unsigned grid = unsigned(std::min(pt.n, sm_count(ctx)));
+  SL_DISPATCH(degree, dist,
+              (pipe_kernel(k_gather_pipe<DEG, DIST, MODE>)<<<grid, PIPE_THREADS, PIPE_SMEM,
+                                                             ctx->stream>>>(
+                  g, src_of<DIST>(f, gh), boxes, tmD, tmA, aux ? 1 : 0, out, half, last, mt_out,
+                  zm, pt)));
+}
 
 struct CharsInfo {
   bool identity;
@@ -974,7 +1063,13 @@ void interp_sweep(vreg_ctx ctx, const Slab& s, const float* f, const float* disp
   const dim3 grid = sl_grid(s), block(BX, BY);
   if (use_tile()) {
     const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
+    const bool pipe = use_pipe(s, {f, disp3, q, out});
     gather_tiles(ctx, s, f, ci.G, dist, gh, [&](TileZ zm, int nz) {
+      if (pipe) {
+        gather_pipe<0>(ctx, s, degree, dist, f, gh, tl.boxes, disp3, q, out, 0.f, 0, nullptr, zm,
+                       nz);
+        return;
+      }
       SL_DISPATCH(degree, dist,
                   (tile_kernel(k_gather_tile<DEG, DIST, 0>)<<<tile_grid_nz(s, nz), TILE_THREADS,
                                                                tl.smem, ctx->stream>>>(
@@ -1170,7 +1265,14 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
       p2p_signal(ctx, P2P_DONE, ctx->pdone);        // done reading the neighbours' w_t
     } else if (fused_u) {
       const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
+      const float* ut = u + size_t(t) * N;
+      const bool pipe = use_pipe(s, {wt, disp3, ut, wn, mo});
       gather_tiles(ctx, s, wt, ci.G, dist, gh, [&](TileZ zm, int nz) {
+        if (pipe) {
+          gather_pipe<2>(ctx, s, degree, dist, wt, gh, tl.boxes, disp3, ut, wn, half,
+                         last ? 1 : 0, mo, zm, nz);
+          return;
+        }
         SL_DISPATCH(degree, dist,
                     (tile_kernel(k_gather_tile<DEG, DIST, 2>)<<<tile_grid_nz(s, nz), TILE_THREADS,
                                                                  tl.smem, ctx->stream>>>(
@@ -1209,7 +1311,7 @@ void sl_transpose_sweeps(vreg_ctx ctx, const Slab& s, const float* disp3, int fl
   // max|psi_t| bits per slice: each sweep's finish hands the next its scale
   unsigned* mx = nullptr;
   if (ctx->deterministic && use_tile() && !ci.identity) {
-    mx = static_cast<unsigned*>(workspace(ctx, "sc_chain", 64 * sizeof(unsigned)));
+    mx = static_cast<unsigned*>(workspace(ctx, "sc_chain", size_t(s.nt + 1) * sizeof(unsigned)));
     VB_CUDA(cudaMemsetAsync(mx, 0, size_t(s.nt + 1) * sizeof(unsigned), ctx->stream));
     k_maxabs_bits<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, psi + size_t(s.nt) * N,
                                                                mx + s.nt);
@@ -1349,6 +1451,11 @@ void sl_source_factor(vreg_ctx ctx, const Slab& s, const float* d, const float* 
   const float half = float(0.5 * s.dt());
   if (use_tile() && !ci.identity) {
     const TileLaunch tl = tile_table(ctx, s, disp_bwd3, degree, false);
+    if (use_pipe(s, {d, disp_bwd3, q})) {
+      gather_pipe<3>(ctx, s, degree, dist, d, gh, tl.boxes, disp_bwd3, d, q, half, 0, nullptr,
+                     kAllLayers, (s.n1l + TT1 - 1) / TT1);
+      return;
+    }
     SL_DISPATCH(degree, dist,
                 (tile_kernel(k_gather_tile<DEG, DIST, 3>)<<<tile_grid(s), TILE_THREADS, tl.smem,
                                                              ctx->stream>>>(
