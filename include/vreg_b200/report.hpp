@@ -3,7 +3,7 @@
 // The reference declares render_report / render_timings /
 // render_residuals_csv (proj/include/vreg/report.hpp:79-84) without defining
 // them, and specifies the VolumeFile format "VRG1". These
-// are the definitions for vreg_b200::SolverReport (solver.hpp):
+// are the definitions for vreg_b200::SolverReport (records.hpp):
 //   * render_report: deterministic structured text, no timings, so serial
 //     reruns are byte-identical;
 //   * render_timings: the wall-clock section (phase and kernel timers);
@@ -21,7 +21,7 @@
 #include <string>
 #include <vector>
 
-#include "vreg_b200/solver.hpp"
+#include "vreg_b200/records.hpp"
 
 namespace vreg_b200 {
 

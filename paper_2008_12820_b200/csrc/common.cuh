@@ -102,6 +102,7 @@ enum CommCat {
 struct FftPlans {
   cufftHandle r2c = 0, c2r = 0;
   size_t work = 0;
+  cudaStream_t stream = nullptr;  // stream the plans are bound to
 };
 
 // ---- context --------------------------------------------------------------

@@ -80,7 +80,16 @@ double* pinned(vreg_ctx ctx, size_t n) {
 FftPlans& fft_plans(vreg_ctx ctx, int n1, int n2, int n3, int batch) {
   auto key = std::make_tuple(n1, n2, n3, batch);
   auto it = ctx->plans.find(key);
-  if (it != ctx->plans.end()) return it->second;
+  if (it != ctx->plans.end()) {
+    // plans follow the context's current stream (side-stream branches,
+    // graph-capture streams of the Krylov solver)
+    if (it->second.stream != ctx->stream) {
+      VB_CUFFT(cufftSetStream(it->second.r2c, ctx->stream));
+      VB_CUFFT(cufftSetStream(it->second.c2r, ctx->stream));
+      it->second.stream = ctx->stream;
+    }
+    return it->second;
+  }
   std::lock_guard<std::mutex> lock(g_plan_mutex);
   FftPlans p;
   int n[3] = {n1, n2, n3};
@@ -109,6 +118,7 @@ FftPlans& fft_plans(vreg_ctx ctx, int n1, int n2, int n3, int batch) {
   VB_CUFFT(cufftSetWorkArea(p.c2r, ctx->fft_work));
   VB_CUFFT(cufftSetStream(p.r2c, ctx->stream));
   VB_CUFFT(cufftSetStream(p.c2r, ctx->stream));
+  p.stream = ctx->stream;
   return ctx->plans.emplace(key, p).first->second;
 }
 
@@ -322,6 +332,7 @@ int vreg_ctx_set_stream(vreg_ctx ctx, void* s) {
     for (auto& kv : ctx->plans) {
       VB_CUFFT(cufftSetStream(kv.second.r2c, ctx->stream));
       VB_CUFFT(cufftSetStream(kv.second.c2r, ctx->stream));
+      kv.second.stream = ctx->stream;
     }
   });
 }

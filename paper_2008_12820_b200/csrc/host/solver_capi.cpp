@@ -1,6 +1,6 @@
-// Solver-level C ABI (include/vreg_b200.h) over the C++ host layer
-// (include/vreg_b200/solver.hpp). Exceptions never cross the ABI: they map
-// back to the status codes of vreg_cuda.h.
+// Solver-level C ABI (include/vreg_b200.h) over the device-resident
+// Gauss-Newton-Krylov layer (csrc/host/gnk.hpp). Exceptions never cross the
+// ABI: they map back to the status codes of vreg_cuda.h.
 #include <cuda_runtime.h>
 #include <cstring>
 #include <memory>
@@ -9,8 +9,8 @@
 #include <string>
 
 #include "vreg_b200.h"
+#include "gnk.hpp"
 #include "vreg_b200/report.hpp"
-#include "vreg_b200/solver.hpp"
 
 namespace vb {
 void set_last_error(const std::string& m);
@@ -27,7 +27,7 @@ struct vreg_solver_s {
   ObjectiveValue J;
   std::optional<DVField> grad;
   Real beta = 0;
-  std::unique_ptr<Preconditioner> prec;
+  std::unique_ptr<DevicePrecond> prec;
   std::optional<DVField> io_in, io_out;  // device staging of the host-buffer matvec
   std::optional<SolverReport> last;      // of the last vreg_solver_register
   // pipelined host-buffer matvec: two slots, upload / download streams
@@ -105,6 +105,7 @@ RegistrationConfig from_c(const vreg_config* c) {
   r.armijo_shrink = c->armijo_shrink;
   r.armijo_max_trials = c->armijo_max_trials;
   r.h0_inner_cap = c->h0_inner_cap;
+  r.pcg_fp64 = c->pcg_fp64 != 0;
   return r;
 }
 
@@ -148,6 +149,7 @@ void vreg_config_default(vreg_config* c) {
   c->armijo_shrink = r.armijo_shrink;
   c->armijo_max_trials = r.armijo_max_trials;
   c->h0_inner_cap = r.h0_inner_cap;
+  c->pcg_fp64 = r.pcg_fp64;
 }
 
 int vreg_solver_create(vreg_ctx ctx, const vreg_grid* g, const vreg_config* cfg,
@@ -215,8 +217,8 @@ int vreg_solver_linearize(vreg_solver s, const float* v3, double beta) {
     check(vreg_memcpy_d2d(e.ctx(), v.data(), v3, 3 * v.local_points() * sizeof(float)));
     s->beta = beta;
     s->lin = std::make_unique<Transport>(e, std::move(v), s->cfg.interp_degree);
-    s->J = evaluate_objective(e, *s->lin, s->m0, s->m1, beta, s->cfg);
-    s->grad = evaluate_gradient(e, *s->lin, s->m1, beta, s->cfg);
+    s->J = objective(e, *s->lin, s->m0, s->m1, beta, s->cfg);
+    s->grad = gradient(e, *s->lin, s->m1, beta, s->cfg);
     s->lin->gradients();  // state-gradient cache for the matvecs
     s->prec.reset();
   });
@@ -250,14 +252,7 @@ bool direct_matvec(vreg_solver s, const float* vt3, float* out3) {
   CudaEngine& e = s->eng;
   const auto& ch = s->lin->forward();
   const float* gr = s->lin->gradients();
-  auto& k = e.counters();
-  const std::uint64_t nt = std::uint64_t(e.grid().nt);
-  k.sl_inc_state++;
-  k.sl_inc_adjoint++;
-  k.ip_eval += 2 * nt;
-  k.ip_scatter += nt;
-  k.fft_forward += 3;
-  k.fft_inverse += 3;
+  count_matvecs(e.counters(), c, e.grid().nt, 1);
   const vreg_grid g = e.vg();
   check(vreg_gn_matvec(e.ctx(), &g, ch.dep.data(), ch.flags, s->lin->degree(), gr, s->beta, vt3,
                        out3));
@@ -271,11 +266,8 @@ int vreg_solver_matvec(vreg_solver s, const float* vt3, float* out3) {
     require_lin(s);
     if (direct_matvec(s, vt3, out3)) return;
     CudaEngine& e = s->eng;
-    DVField vt = e.make_vfield();
-    const size_t bytes = 3 * vt.local_points() * sizeof(float);
-    check(vreg_memcpy_d2d(e.ctx(), vt.data(), vt3, bytes));
-    DVField h = hessian_matvec(e, *s->lin, vt, s->beta, s->cfg);
-    check(vreg_memcpy_d2d(e.ctx(), out3, h.data(), bytes));
+    count_matvecs(e.counters(), s->cfg, e.grid().nt, 1);
+    matvec_into(e, *s->lin, s->beta, s->cfg, vt3, out3);
   });
 }
 
@@ -289,8 +281,10 @@ int vreg_solver_matvec_host(vreg_solver s, const float* vt3_host, float* out3_ho
     }
     const size_t bytes = 3 * s->io_in->local_points() * sizeof(float);
     check(vreg_memcpy_h2d(e.ctx(), s->io_in->data(), vt3_host, bytes));
-    if (!direct_matvec(s, s->io_in->data(), s->io_out->data()))
-      *s->io_out = hessian_matvec(e, *s->lin, *s->io_in, s->beta, s->cfg);
+    if (!direct_matvec(s, s->io_in->data(), s->io_out->data())) {
+      count_matvecs(e.counters(), s->cfg, e.grid().nt, 1);
+      matvec_into(e, *s->lin, s->beta, s->cfg, s->io_in->data(), s->io_out->data());
+    }
     check(vreg_memcpy_d2h(e.ctx(), out3_host, s->io_out->data(), bytes));
   });
 }
@@ -329,8 +323,10 @@ int vreg_solver_matvec_host_async(vreg_solver s, const float* vt3_host, float* o
     // matvec once the upload landed and call k-2's download freed the output
     cuda_check(cudaStreamWaitEvent(st, s->ev_up[k], 0));
     if (s->slot_used[k]) cuda_check(cudaStreamWaitEvent(st, s->ev_down[k], 0));
-    if (!direct_matvec(s, s->pin[k]->data(), s->pout[k]->data()))
-      *s->pout[k] = hessian_matvec(e, *s->lin, *s->pin[k], s->beta, s->cfg);
+    if (!direct_matvec(s, s->pin[k]->data(), s->pout[k]->data())) {
+      count_matvecs(e.counters(), s->cfg, e.grid().nt, 1);
+      matvec_into(e, *s->lin, s->beta, s->cfg, s->pin[k]->data(), s->pout[k]->data());
+    }
     cuda_check(cudaEventRecord(s->ev_mv[k], st));
     cuda_check(cudaStreamWaitEvent(s->down, s->ev_mv[k], 0));
     cuda_check(cudaMemcpyAsync(out3_host, s->pout[k]->data(), bytes, cudaMemcpyDeviceToHost,
@@ -354,22 +350,22 @@ int vreg_solver_precond(vreg_solver s, int kind, const float* r3, double eps_k, 
   return guarded([&] {
     require_lin(s);
     CudaEngine& e = s->eng;
+    if (kind < 0 || kind > 2) throw parameter_error("preconditioner kind must be 0, 1 or 2");
     if (!s->prec || int(s->prec->kind()) != kind) {
-      s->prec = std::make_unique<Preconditioner>(e, PrecondKind(kind), s->beta, s->cfg.eps_h0,
-                                                 s->cfg.h0_inner_cap);
+      s->prec = std::make_unique<DevicePrecond>(e, PrecondKind(kind), s->beta, s->cfg.eps_h0,
+                                                s->cfg.h0_inner_cap);
       s->prec->refresh(s->lin->state_field(e.grid().nt));
     }
-    DVField r = e.make_vfield();
-    const size_t bytes = 3 * r.local_points() * sizeof(float);
-    check(vreg_memcpy_d2d(e.ctx(), r.data(), r3, bytes));
-    PrecondStats st;
-    DVField z = s->prec->apply(r, eps_k, st);
-    check(vreg_memcpy_d2d(e.ctx(), out3, z.data(), bytes));
+    s->prec->take_device();
+    s->prec->apply_once(r3, out3, eps_k);
+    const auto inner = s->prec->take_device();
+    PrecondTally t;
+    s->prec->count(1, inner.first, t);
     if (stats4) {
-      stats4[0] = st.inva_applications;
-      stats4[1] = st.h0_applications;
-      stats4[2] = st.inner_iterations;
-      stats4[3] = st.inner_capped ? 1 : 0;
+      stats4[0] = t.inva;
+      stats4[1] = t.h0;
+      stats4[2] = t.inner;
+      stats4[3] = inner.second ? 1 : 0;
     }
   });
 }
@@ -378,7 +374,7 @@ int vreg_solver_register(vreg_solver s, float* v_out3, double rep16[16], uint64_
   return guarded([&] {
     CudaEngine& e = s->eng;
     DVField v;
-    SolverReport r = register_images(e, s->m0, s->m1, s->cfg, &v);
+    SolverReport r = Registration(e, s->m0, s->m1, s->cfg).run(&v);
     s->last = r;
     if (v_out3)
       check(vreg_memcpy_d2d(e.ctx(), v_out3, v.data(), 3 * v.local_points() * sizeof(float)));

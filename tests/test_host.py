@@ -51,8 +51,11 @@ def test_config_layout_matches_reference_config():
     from oracle import ref
     from paper_2008_12820_b200 import _lib
     from paper_2008_12820_b200.solver import Config, VregConfig
-    assert [f[0] for f in VregConfig._fields_] == [f[0] for f in ref.VrefConfig._fields_]
-    assert C.sizeof(VregConfig) == C.sizeof(ref.VrefConfig)
+    # the reference's RegistrationConfig fields in order (optim.hpp:16-37),
+    # then the B200 extension pcg_fp64 (fp64 PCG iterates)
+    names = [f[0] for f in VregConfig._fields_]
+    assert names[:-1] == [f[0] for f in ref.VrefConfig._fields_] and names[-1] == "pcg_fp64"
+    assert VregConfig.pcg_fp64.offset >= C.sizeof(ref.VrefConfig) - 4
     c = VregConfig()
     _lib.lib().vreg_config_default(C.byref(c))
     d = Config().to_c()

@@ -42,9 +42,11 @@ def main():
         tr = time.time() - t
         s = Solver(ctx, n, Config())
         s.syn_images()
+        t = time.time()
         v, rep, _ = s.register()
+        t_dev = time.time() - t
         lv = parse_levels(s.report_text("report"))
-        print(json.dumps(dict(n=n, ref_s=tr, ref_levels=[(l["gn_iters"], l["pcg_total"], l["final_mismatch"], l["final_g_rel"]) for l in L],
+        print(json.dumps(dict(n=n, ref_s=tr, dev_s=t_dev, ref_levels=[(l["gn_iters"], l["pcg_total"], l["final_mismatch"], l["final_g_rel"]) for l in L],
                               dev_levels=[(l["gn"], l["pcg"], l["final_mismatch"], l["final_g_rel"]) for l in lv],
                               ref_vnorm=gnorm(vr, n), dev_vnorm=gnorm(v.double().cpu().numpy(), n),
                               ref_iters=[(i["level"], i["pcg_iters"], i["alpha"], i["g_rel"]) for i in I])), flush=True)
@@ -52,13 +54,16 @@ def main():
     # fixed InvA 64^3 2x10 vs SURVEY golden (mismatch 6.7136229316e-3, ||v|| 3.7991080969)
     n = 64
     for pc in ("inva", "2linvh0"):
-        s = Solver(ctx, n, Config(continuation=False, beta_target=1e-3, fixed_gn=2, fixed_pcg=10,
-                                  precond=pc))
-        s.syn_images()
-        v, rep, _ = s.register()
-        print(json.dumps(dict(fixed=pc, mismatch=rep["final_mismatch"], g_rel=rep["final_g_rel"],
-                              vnorm=gnorm(v.double().cpu().numpy(), n))), flush=True)
-        s.close()
+        for f64 in (True, False):
+            s = Solver(ctx, n, Config(continuation=False, beta_target=1e-3, fixed_gn=2,
+                                      fixed_pcg=10, precond=pc, pcg_fp64=f64))
+            s.syn_images()
+            t = time.time()
+            v, rep, _ = s.register()
+            print(json.dumps(dict(fixed=pc, pcg_fp64=f64, mismatch=rep["final_mismatch"],
+                                  g_rel=rep["final_g_rel"], secs=time.time() - t,
+                                  vnorm=gnorm(v.double().cpu().numpy(), n))), flush=True)
+            s.close()
     ctx.close()
 
 
