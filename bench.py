@@ -163,22 +163,31 @@ def ncu_smem_wavefronts():
 
 # --------------------------------------------------------------- CPU legs ----
 
-def cpu_reference_sample(n=128, matvecs=1):
-    """The UNMODIFIED reference (oracle/_ref, fp64, single-threaded: it has no
-    threading) on the host: `matvecs` GN matvecs at the SYN linearisation
-    point on an n^3 grid. Returns (Mvox*matvec/s, seconds, kind, sample)."""
-    import numpy as np
+def _ref_session(n):
+    """The UNMODIFIED reference (oracle/_ref) at the bench linearisation point
+    (SYN, v = 0.5 v_syn, vt = -g). Returns (session, vt)."""
+    from oracle import ref
+    m0, v, m1 = ref.syn(n, NT, 3)
+    s = ref.Session(m0, m1, 0.5 * v, BETA, ref.Config(continuation=False, beta_target=BETA))
+    return s, -s.gradient()
+
+
+def cpu_reference_sample(n=256, matvecs=1):
+    """`matvecs` GN matvecs of the compiled reference (fp64; single-threaded:
+    it has no OpenMP or threads) on the host at the benchmark grid. Returns
+    (Mvox*matvec/s, seconds, kind, sample, reference KernelTimers per matvec)."""
     from oracle import ref
     if ref.available():
-        m0, v, m1 = ref.syn(n, NT, 3)
-        s = ref.Session(m0, m1, 0.5 * v, BETA, ref.Config(continuation=False, beta_target=BETA))
-        vt = -s.gradient()
+        s, vt = _ref_session(n)
+        t_before = s.timers()
         t0 = time.perf_counter()
         for _ in range(matvecs):
             s.matvec(vt)
         dt = time.perf_counter() - t0
+        t_after = s.timers()
+        timers = {k: (t_after[k] - t_before[k]) / matvecs for k in t_after}
         return n ** 3 * matvecs / dt / 1e6, dt, "reference", \
-            f"{matvecs} GN matvec(s) of the compiled reference at {n}^3 (fp64, 1 thread)"
+            f"{matvecs} GN matvec(s) of the compiled reference at {n}^3 (fp64, 1 thread)", timers
     from oracle import vreg_np as O
     n = min(n, 64)
     m0 = O.syn_template((n,) * 3)
@@ -191,42 +200,51 @@ def cpu_reference_sample(n=128, matvecs=1):
         L.matvec(-L.g)
     dt = time.perf_counter() - t0
     return n ** 3 * matvecs / dt / 1e6, dt, "port", \
-        f"{matvecs} GN matvec(s) of the numpy restatement at {n}^3 (fp64)"
+        f"{matvecs} GN matvec(s) of the numpy restatement at {n}^3 (fp64)", None
 
 
 def run_reference(args):
+    """Reference arm: the compiled reference's own GN matvec
+    (detail::hessian_matvec_with, optim.hpp:115-137) on the host, one matvec
+    of the benchmark grid per step (the same config as our arm, N = 1)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n = 128
-    vals = []
-    # warm-up steps are part of the contract; each step is one 128^3 matvec
     from oracle import ref
-    import numpy as np
+    nx, ny, nz = (args.size,) * 3 if args.gpus == 1 else weak_grid(args.size, args.gpus)
+    n = args.size
+    same = args.gpus == 1
     if ref.available():
-        m0, v, m1 = ref.syn(n, NT, 3)
-        s = ref.Session(m0, m1, 0.5 * v, BETA, ref.Config(continuation=False, beta_target=BETA))
-        vt = -s.gradient()
+        s, vt = _ref_session(n)
         for _ in range(args.warmup):
             s.matvec(vt)
+        t_before = s.timers()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             s.matvec(vt)
         dt = time.perf_counter() - t0
-        kind, sample = "reference", f"{args.steps} GN matvecs of the compiled reference at {n}^3 (fp64, 1 thread; the reference has no threading)"
+        t_after = s.timers()
+        timers = {k: round((t_after[k] - t_before[k]) / args.steps, 4) for k in t_after}
+        kind = "reference"
+        sample = (f"{args.steps} GN matvecs of the compiled reference at {n}^3 (fp64, 1 thread; "
+                  "the reference has no threading)")
     else:
-        val, dt, kind, sample = cpu_reference_sample(64, args.steps)
-        n = 64
+        val, dt, kind, sample, timers = cpu_reference_sample(64, args.steps)
+        n, same = 64, False
     value = n ** 3 * args.steps / dt / 1e6
-    nx, ny, nz = (args.size,) * 3 if args.gpus == 1 else weak_grid(args.size, args.gpus)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"SYN {nx}x{ny}x{nz} GN Hessian matvec (sample at {n}^3 on CPU)",
+        "config": {"workload": f"SYN {nx}x{ny}x{nz} GN Hessian matvec" +
+                   ("" if same else f" (per-GPU {n}^3 sample on the host)"),
                    "grid": [nx, ny, nz], "nt": NT, "interp_degree": 3, "beta": BETA},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample},
+        "same_config_as_gpu_arm": same,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample,
+                         "host_cores": os.cpu_count()},
+        "reference_kernel_timers_s_per_matvec": timers,
+        "fft_column": "FFTW3-API shim (oracle/shim/fftw_shim.c; FFTW3 is not installed)",
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -456,9 +474,10 @@ def run_ours(args):
         fft_s = t_after["fft"] - t_before["fft"]
         cpu = None
         if world == 1 and not args.no_cpu:
-            val, dt, kind, sample = cpu_reference_sample(128, 1)
+            val, dt, kind, sample, timers = cpu_reference_sample(dims[0] if dims[0] == dims[1] == dims[2] else 64, 1)
             cpu = {"value": val, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample,
-                   "seconds": dt, "host_cores": os.cpu_count()}
+                   "seconds": dt, "host_cores": os.cpu_count(),
+                   "reference_kernel_timers_s": timers, "fft_column": "FFTW3-API shim"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -486,7 +505,8 @@ def run_ours(args):
                     "ghost_interp_bytes", "scatter_points_bytes", "fft_transpose_bytes",
                     "ghost_fd_bytes", "reduce_bytes")) / args.steps / 900e9 * 1e3,
                 "comm_timer_ms": round(sum((t_after[k] - t_before[k]) for k in (
-                    "interp_comm", "scatter_comm", "transpose_comm")) / args.steps * 1e3, 4)},
+                    "interp_comm", "scatter_comm", "transpose_comm")) / args.steps * 1e3, 4),
+                **nvlink_roofline(c_before, c_after, t_before, t_after, args.steps)},
             "timer_ms_per_step": {k: round((t_after[k] - t_before[k]) / args.steps * 1e3, 4)
                                   for k in t_after if t_after[k] != t_before[k]},
             "kernel_share": share,
@@ -507,6 +527,25 @@ def run_ours(args):
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+NVLINK_PEER_GBS = 770.0   # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+def nvlink_roofline(c0, c1, t0, t1, steps):
+    """NVLink roofline of the exchanges: bytes each GPU sends per matvec over
+    the time the comm timers saw them take (halos, reverse halos, regulariser
+    transposes), against the measured 770 GB/s peer copy per direction."""
+    keys_b = ("ghost_interp_bytes", "scatter_points_bytes", "fft_transpose_bytes",
+              "ghost_fd_bytes", "reduce_bytes")
+    keys_t = ("interp_comm", "scatter_comm", "transpose_comm")
+    b = sum(c1[k] - c0[k] for k in keys_b) / steps
+    t = sum(t1[k] - t0[k] for k in keys_t) / steps
+    if t <= 0:
+        return {}
+    ach = b / t / 1e9
+    return {"achieved_gbs": ach, "peak_gbs": NVLINK_PEER_GBS, "peak_kind": "measured peer copy",
+            "frac": ach / NVLINK_PEER_GBS}
 
 
 _JSON_FD = None

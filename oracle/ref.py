@@ -348,7 +348,8 @@ def register(m0, m1, cfg: Config):
 
 LEVEL_KEYS = ["beta", "inva", "switched", "gn_iters", "pcg_total", "final_mismatch",
               "final_g_rel", "converged"]
-ITER_KEYS = ["level", "objective", "mismatch", "g_rel", "eps_k", "alpha", "pcg_iters"]
+ITER_KEYS = ["level", "objective", "mismatch", "g_rel", "eps_k", "alpha", "pcg_iters",
+             "h0_inner_iters"]
 
 
 def register_levels(m0, m1, cfg: Config):
@@ -358,7 +359,7 @@ def register_levels(m0, m1, cfg: Config):
     c = cfg.to_c()
     v = np.zeros((3,) + shape)
     lev = np.zeros((64, 8))
-    its = np.zeros((1024, 7))
+    its = np.zeros((1024, 8))
     nl, ni = C.c_int(0), C.c_int(0)
     m0c = np.ascontiguousarray(m0, dtype=np.float64)
     m1c = np.ascontiguousarray(m1, dtype=np.float64)
@@ -367,3 +368,17 @@ def register_levels(m0, m1, cfg: Config):
     levels = [dict(zip(LEVEL_KEYS, r.tolist())) for r in lev[:nl.value]]
     iters = [dict(zip(ITER_KEYS, r.tolist())) for r in its[:min(ni.value, 1024)]]
     return v, levels, iters
+
+
+def register_residuals(m0, m1, cfg: Config):
+    """PCG relative-residual histories of register_images: rows (level,
+    gn iteration, pcg iteration, relres) as render_residuals_csv."""
+    shape = m0.shape
+    c = cfg.to_c()
+    rows = np.zeros((8192, 4))
+    n = C.c_int(0)
+    m0c = np.ascontiguousarray(m0, dtype=np.float64)
+    m1c = np.ascontiguousarray(m1, dtype=np.float64)
+    _chk(lib().vref_register_residuals(*_dims(shape), C.byref(c), _p(m0c), _p(m1c), _p(rows),
+                                       8192, C.byref(n)))
+    return rows[:min(n.value, 8192)]

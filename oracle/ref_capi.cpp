@@ -431,8 +431,9 @@ int vref_register(int n1, int n2, int n3, const vref_config* c,
 // register_images (optim.hpp:308-347) with the per-level / per-GN-iteration
 // records of its SolverReport (report.hpp:12-78): level rows of 8 doubles
 // (beta, pc is inva, switched, gn_iters, pcg_total, final_mismatch,
-// final_g_rel, converged) and GN rows of 7 (level, objective, mismatch,
-// g_rel, eps_k, alpha, pcg_iters). Capacities in rows; counts returned.
+// final_g_rel, converged) and GN rows of 8 (level, objective, mismatch,
+// g_rel, eps_k, alpha, pcg_iters, h0_inner_iters). Capacities in rows;
+// counts returned.
 int vref_register_levels(int n1, int n2, int n3, const vref_config* c, const double* m0,
                          const double* m1, double* v_out3, double* lev, int lev_cap,
                          int* nlev, double* its, int its_cap, int* nits) {
@@ -458,7 +459,7 @@ int vref_register_levels(int n1, int n2, int n3, const vref_config* c, const dou
       }
       for (const GnIterRecord& it : l.iters) {
         if (I < its_cap) {
-          double* o = its + 7 * I;
+          double* o = its + 8 * I;
           o[0] = L;
           o[1] = it.objective;
           o[2] = it.mismatch;
@@ -466,6 +467,7 @@ int vref_register_levels(int n1, int n2, int n3, const vref_config* c, const dou
           o[4] = it.eps_k;
           o[5] = it.alpha;
           o[6] = it.pcg_iters;
+          o[7] = double(it.h0_inner_iters);
         }
         ++I;
       }
@@ -473,6 +475,33 @@ int vref_register_levels(int n1, int n2, int n3, const vref_config* c, const dou
     }
     *nlev = L;
     *nits = I;
+  })
+}
+
+// PCG relative-residual histories of the last register_levels-style run:
+// (level, gn index, pcg iteration, rel. residual) rows, as render_residuals_csv.
+int vref_register_residuals(int n1, int n2, int n3, const vref_config* c, const double* m0,
+                            const double* m1, double* rows4, int cap, int* nrows) {
+  GUARD({
+    RegistrationConfig cfg = to_cfg(c);
+    Grid3 g = Grid3::make(n1, n2, n3, cfg.nt);
+    SerialEngine eng = SerialEngine::create(g);
+    SolverReport r = register_images(eng, load(g, m0), load(g, m1), cfg, nullptr);
+    int n = 0;
+    for (size_t li = 0; li < r.levels.size(); ++li)
+      for (size_t k = 0; k < r.levels[li].iters.size(); ++k) {
+        const auto& h = r.levels[li].iters[k].pcg_relres;
+        for (size_t j = 0; j < h.size(); ++j) {
+          if (n < cap) {
+            rows4[4 * n] = double(li);
+            rows4[4 * n + 1] = double(k + 1);
+            rows4[4 * n + 2] = double(j);
+            rows4[4 * n + 3] = h[j];
+          }
+          ++n;
+        }
+      }
+    *nrows = n;
   })
 }
 

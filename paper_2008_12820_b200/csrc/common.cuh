@@ -135,15 +135,6 @@ struct vreg_ctx_s {
   std::vector<float*> peer_recv;
   size_t xbytes = 0;
   int* xflag = nullptr;
-  // peer arena of the fused multi-GPU SL sweeps (p2p.cu): IPC-mapped buffers
-  // the ring neighbours read (ghost planes) and add into (reverse halo)
-  // directly, plus the flag words of the release/acquire handshakes
-  char* parena = nullptr;
-  size_t parena_bytes = 0;
-  char* parena_prev = nullptr;
-  char* parena_next = nullptr;
-  uint64_t pseq = 0;       // handshake sequence number (same program order on all ranks)
-  uint64_t pdone = 0;      // last DONE_W sequence of the previous inc-state solve
 
   // FFT plans keyed by (n1, n2, n3, batch); one shared work area
   std::map<std::tuple<int, int, int, int>, vb::FftPlans> plans;
@@ -259,18 +250,6 @@ Ghosts halo_exchange(vreg_ctx ctx, const Slab& s, const float* f, int G,
 GhostAcc ghost_accumulators(vreg_ctx ctx, const Slab& s, int G, const char* slot);
 // Reverse halo: ship the ghost accumulators to their owners and add them
 // into the owners' boundary planes of out.
-// ---- fused multi-GPU SL sweeps over peer memory (p2p.cu) ----
-enum P2PFlag { P2P_READY = 0, P2P_DONE = 1, P2P_ZEROED = 2, P2P_ADDED = 3 };
-bool p2p_enabled(vreg_ctx ctx);
-// data region of the arena (>= bytes), created / regrown collectively
-char* p2p_data(vreg_ctx ctx, size_t bytes);
-// the same offset in the ring neighbours' arenas
-const char* p2p_peer(vreg_ctx ctx, const void* local, bool next);
-uint64_t p2p_seq(vreg_ctx ctx);
-// stream-ordered release of `seq` into both neighbours' flag `type`
-void p2p_signal(vreg_ctx ctx, int type, uint64_t seq);
-// stream-ordered acquire: both neighbours reached `seq` on flag `type`
-void p2p_wait(vreg_ctx ctx, int type, uint64_t seq);
 
 // Reverse halo add in two halves so the exchange can run on another stream:
 // send the ghost accumulators / receive the neighbours' (top, bot), then add.

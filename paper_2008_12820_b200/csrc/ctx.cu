@@ -273,10 +273,6 @@ int vreg_ctx_destroy(vreg_ctx ctx) {
     for (int i = 0; i < 2; ++i)
       if (ctx->xbuf[i]) cudaFree(ctx->xbuf[i]);
     if (ctx->xflag) cudaFree(ctx->xflag);
-    if (ctx->parena_prev) cudaIpcCloseMemHandle(ctx->parena_prev);
-    if (ctx->parena_next && ctx->parena_next != ctx->parena_prev)
-      cudaIpcCloseMemHandle(ctx->parena_next);
-    if (ctx->parena) cudaFree(ctx->parena);
     if (ctx->fft_comm) ncclCommDestroy(ctx->fft_comm);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);

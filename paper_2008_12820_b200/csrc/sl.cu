@@ -11,7 +11,6 @@
 
 #include "common.cuh"
 #include "sl_common.cuh"
-#include "sl_quad.cuh"
 #include "sl_tile.cuh"
 #include "sl_pipe.cuh"
 
@@ -44,58 +43,6 @@ inline Geo geo_of(const Slab& s) {
   const int i = blockIdx.z;                                \
   if (k >= g.n3 || j >= g.n2) return;                      \
   const size_t p = (size_t(i) * g.n2 + j) * g.n3 + k;
-
-template <int DEG, bool DIST>
-__global__ void __launch_bounds__(BX* BY) k_interp(Geo g, SrcField<DIST> src,
-                                                   const float* __restrict__ D,
-                                                   float* __restrict__ out) {
-  SL_INDEX
-  Stencil<DEG> st;
-  st.template build<DIST>(g, i, j, k, D[p], D[g.N + p], D[2 * g.N + p]);
-  out[p] = st.gather(g, src);
-}
-
-// out = I[f] .* q (adjoint sweep step: interp then hadamard, transport.hpp:115-117)
-template <int DEG, bool DIST>
-__global__ void __launch_bounds__(BX* BY) k_interp_mul(Geo g, SrcField<DIST> src,
-                                                       const float* __restrict__ D,
-                                                       const float* __restrict__ q,
-                                                       float* __restrict__ out) {
-  SL_INDEX
-  Stencil<DEG> st;
-  st.template build<DIST>(g, i, j, k, D[p], D[g.N + p], D[2 * g.N + p]);
-  out[p] = st.gather(g, src) * q[p];
-}
-
-template <int DEG, bool DIST>
-__global__ void __launch_bounds__(BX* BY) k_scatter(Geo g, DstField<DIST> dst,
-                                                    const float* __restrict__ D,
-                                                    const float* __restrict__ z) {
-  SL_INDEX
-  const float zp = z[p];
-  if (zp == 0.0f) return;  // contributes nothing
-  Stencil<DEG> st;
-  st.template build<DIST>(g, i, j, k, D[p], D[g.N + p], D[2 * g.N + p]);
-  st.scatter(g, dst, zp);
-}
-
-// RK2: mid = -dt/h v (grid units); vs = I[v](mid); D = -(dt/2)/h (v + vs).
-template <int DEG, bool DIST>
-__global__ void __launch_bounds__(BX* BY) k_characteristics(
-    Geo g, SrcField<DIST> v1, SrcField<DIST> v2, SrcField<DIST> v3,
-    const float* __restrict__ v, float m1, float m2, float m3, float c1, float c2, float c3,
-    float* __restrict__ D) {
-  SL_INDEX
-  const float a = v[p], b = v[g.N + p], c = v[2 * g.N + p];
-  Stencil<DEG> st;
-  st.template build<DIST>(g, i, j, k, m1 * a, m2 * b, m3 * c);
-  const float va = st.gather(g, v1);
-  const float vb = st.gather(g, v2);
-  const float vc = st.gather(g, v3);
-  D[p] = c1 * (a + va);
-  D[g.N + p] = c2 * (b + vb);
-  D[2 * g.N + p] = c3 * (c + vc);
-}
 
 // One fused incremental-state step (transport.hpp:164-179), using linearity
 // of I: w_t = m~_t - dt/2 u_t, I[m~_t] - dt/2 I[u_t] = I[w_t]:
@@ -234,83 +181,6 @@ __global__ void __launch_bounds__(BX* BY) k_source_factor(Geo g, SrcField<DIST> 
     dd = st.gather(g, dsrc);
   }
   q[p] = (1.0f + half * dd) / (1.0f - half * dsrc.f[p]);
-}
-
-// ---- quad (4 x3-points per thread) variants, used when n3 % 4 == 0 --------
-
-#define SLQ_INDEX                                          \
-  const int k0 = 4 * (blockIdx.x * BX + threadIdx.x);      \
-  const int j = blockIdx.y * BY + threadIdx.y;             \
-  const int i = blockIdx.z;                                \
-  if (k0 >= g.n3 || j >= g.n2) return;                     \
-  const size_t p = (size_t(i) * g.n2 + j) * g.n3 + k0;
-
-__device__ __forceinline__ float4 ld4(const float* p) {
-  return __ldg(reinterpret_cast<const float4*>(p));
-}
-__device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
-  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
-}
-
-template <int DEG, bool DIST>
-__global__ void __launch_bounds__(BX* BY) k_interp_q(Geo g, SrcField<DIST> src,
-                                                     const float* __restrict__ D,
-                                                     const float* __restrict__ qf,
-                                                     float* __restrict__ out) {
-  SLQ_INDEX
-  Quad<DEG> Q;
-  Q.build(ld4(D + p), ld4(D + g.N + p), ld4(D + 2 * g.N + p));
-  float r[4];
-  quad_gather(g, src, Q, i, j, k0, r);
-  if (qf) {
-    const float4 m = ld4(qf + p);
-    r[0] *= m.x; r[1] *= m.y; r[2] *= m.z; r[3] *= m.w;
-  }
-  st4(out + p, r[0], r[1], r[2], r[3]);
-}
-
-template <int DEG, bool DIST>
-__global__ void __launch_bounds__(BX* BY) k_scatter_q(Geo g, DstField<DIST> dst,
-                                                      const float* __restrict__ D,
-                                                      const float* __restrict__ z) {
-  SLQ_INDEX
-  const float4 zz = ld4(z + p);
-  if (zz.x == 0.f && zz.y == 0.f && zz.z == 0.f && zz.w == 0.f) return;
-  const float zv[4] = {zz.x, zz.y, zz.z, zz.w};
-  Quad<DEG> Q;
-  Q.build(ld4(D + p), ld4(D + g.N + p), ld4(D + 2 * g.N + p));
-  quad_scatter(g, dst, Q, i, j, k0, zv);
-}
-
-template <int DEG, bool DIST>
-__global__ void __launch_bounds__(BX* BY) k_inc_step_q(Geo g, SrcField<DIST> wsrc,
-                                                       const float* __restrict__ D, int ident,
-                                                       const float* __restrict__ vt,
-                                                       const float* __restrict__ gr, float half,
-                                                       int last, float* __restrict__ w_next,
-                                                       float* __restrict__ mt_out) {
-  SLQ_INDEX
-  float G[4];
-  if (ident) {
-    const float4 w = ld4(wsrc.f + p);
-    G[0] = w.x; G[1] = w.y; G[2] = w.z; G[3] = w.w;
-  } else {
-    Quad<DEG> Q;
-    Q.build(ld4(D + p), ld4(D + g.N + p), ld4(D + 2 * g.N + p));
-    quad_gather(g, wsrc, Q, i, j, k0, G);
-  }
-  const float4 v1 = ld4(vt + p), v2 = ld4(vt + g.N + p), v3 = ld4(vt + 2 * g.N + p);
-  const float4 g1 = ld4(gr + p), g2 = ld4(gr + g.N + p), g3 = ld4(gr + 2 * g.N + p);
-  const float u[4] = {v1.x * g1.x + v2.x * g2.x + v3.x * g3.x, v1.y * g1.y + v2.y * g2.y + v3.y * g3.y,
-                      v1.z * g1.z + v2.z * g2.z + v3.z * g3.z, v1.w * g1.w + v2.w * g2.w + v3.w * g3.w};
-  float m[4], wn[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    m[q] = G[q] - half * u[q];
-    wn[q] = last ? -m[q] : m[q] - half * u[q];
-  }
-  if (mt_out) st4(mt_out + p, m[0], m[1], m[2], m[3]);
-  st4(w_next + p, wn[0], wn[1], wn[2], wn[3]);
 }
 
 // ---- tile-staged variants (sl_tile.cuh) -----------------------------------
@@ -513,8 +383,10 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_chars_tile(
   }
 }
 
-// Default transpose sweep: per-tile power-of-two scale S = 2^(27-e_tile)
-// in the shared int32 box (exact to 2^-28 max|z_tile| per contribution),
+// Default transpose sweep: per-tile power-of-two scale S = 2^(26-e_tile)
+// in the shared int32 box (exact to 2^-27 max|z_tile| per contribution; a
+// cell holds 32 max|z| -- the cubic weights' absolute sum under the
+// compression the adjoint factor allows stays below ~14 max|z|),
 // flushed with float4 REDs. The L2 adds of overlapping tiles land in any
 // order, so the last bits can differ between runs (VREG_DETERMINISTIC=1 /
 // vreg_ctx_set_deterministic selects the fixed-point variant below).
@@ -538,36 +410,41 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_scatter_tile_
     for (int c = threadIdx.x; c < words / 4; c += TILE_THREADS) ib4[c] = make_int4(0, 0, 0, 0);
   }
   float zv[TILE_PPT], d1[TILE_PPT], d2[TILE_PPT], d3[TILE_PPT];
-  float zm = 0.f;
+  unsigned zb = 0u;
 #pragma unroll
   for (int it = 0; it < TILE_PPT; ++it) {
     TILE_PT(it)
     zv[it] = ok ? z[p] : 0.f;
-    zm = fmaxf(zm, fabsf(zv[it]));
+    const float az = fabsf(zv[it]);
+    zb = max(zb, az != az ? 0x7fc00000u : __float_as_uint(az));  // NaN sorts above Inf
     d1[it] = ok ? D[p] : 0.f;
     d2[it] = ok ? D[g.N + p] : 0.f;
     d3[it] = ok ? D[2 * g.N + p] : 0.f;
   }
-  const unsigned zb = __reduce_max_sync(0xffffffffu, __float_as_uint(zm));
+  zb = __reduce_max_sync(0xffffffffu, zb);
   __syncthreads();  // s_zmax initialised, box zeroed
   if ((threadIdx.x & 31) == 0) atomicMax(&s_zmax, zb);
   __syncthreads();
-  zm = __uint_as_float(s_zmax);
+  const float zm = __uint_as_float(s_zmax);
   if (zm == 0.0f) return;  // whole tile contributes nothing
+  // non-finite z: fp32 atomics for the whole tile, so NaN / Inf reach the
+  // output as in the reference's fp32 scatter (a fixed-point box cannot hold them)
+  const bool boxed = fits && zm <= 3.4028235e38f;
   int e = 0;
-  frexpf(zm, &e);  // max |z| < 2^e
-  const float S = ldexpf(1.0f, 27 - e), invS = ldexpf(1.0f, e - 27);
+  if (boxed) frexpf(zm, &e);  // max |z| < 2^e
+  e = max(e, -99);            // scale stays a finite float for tiny tiles
+  const float S = ldexpf(1.0f, 26 - e), invS = ldexpf(1.0f, e - 26);
 #pragma unroll
   for (int it = 0; it < TILE_PPT; ++it) {
     TILE_PT(it)
     if (!ok || zv[it] == 0.0f) continue;
     BoxStencil<DEG> bs;
-    if (fits && bs.build(b, i, j, k, d1[it], d2[it], d3[it]))
+    if (boxed && bs.build(b, i, j, k, d1[it], d2[it], d3[it]))
       bs.scatter(b, ibox, zv[it] * S);
     else
       point_scatter<DEG, DIST>(g, dst, i, j, k, d1[it], d2[it], d3[it], zv[it]);
   }
-  if (fits) {
+  if (boxed) {
     __syncthreads();
     flush_box(g, dst, b, ibox, invS, rows);
   }
@@ -843,30 +720,6 @@ inline Kern tile_kernel(Kern k) {
   return k;
 }
 
-// Tile kernels opt in to 48 KB of dynamic shared memory (VREG_SL_TILE=0
-// selects the per-point kernels, for A/B measurements).
-inline bool use_tile() {
-  static const bool on = [] {
-    const char* e = std::getenv("VREG_SL_TILE");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-inline dim3 slq_grid(const Slab& s) {
-  return dim3(unsigned((s.n3 / 4 + BX - 1) / BX), unsigned((s.n2 + BY - 1) / BY), unsigned(s.n1l));
-}
-
-// Quad kernels (register-blocked, L1/L2 direct) need 16-byte aligned rows;
-// experimental, opt in with VREG_SL_QUAD=1 (and VREG_SL_TILE=0).
-inline bool use_quad(const Slab& s) {
-  static const bool on = [] {
-    const char* e = std::getenv("VREG_SL_QUAD");
-    return e && e[0] == '1';
-  }();
-  return on && s.n3 % 4 == 0;
-}
-
 // ---- TMA pipeline (sl_pipe.cuh) host side ----------------------------------
 
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
@@ -1022,22 +875,6 @@ inline CharsInfo chars_info(vreg_ctx ctx, const Slab& s, const float* disp3, int
   return ci;
 }
 
-// Fused peer-memory sweeps (p2p.cu, VREG_P2P_SL=1): w and psi live in the
-// IPC arena, the tile kernels read ghost planes from / add ghost
-// contributions into the neighbours' copies directly.
-inline bool p2p_sweeps(vreg_ctx ctx, const Slab& s, const CharsInfo& ci) {
-  return ctx->nranks > 1 && !ci.identity && use_tile() && !ctx->deterministic &&
-         s.local() % 4 == 0 && ci.G >= 1 && ci.G <= s.n1l && p2p_enabled(ctx);
-}
-inline bool in_arena(vreg_ctx ctx, const void* p) {
-  const char* c = static_cast<const char*>(p);
-  return ctx->parena && c >= ctx->parena && c < ctx->parena + ctx->parena_bytes;
-}
-template <class T>
-inline T* peer_plane(vreg_ctx ctx, T* local, bool next, size_t plane_off) {
-  return reinterpret_cast<T*>(const_cast<char*>(p2p_peer(ctx, local, next))) + plane_off;
-}
-
 // out = I[f] at disp (optionally .* q)
 void interp_sweep(vreg_ctx ctx, const Slab& s, const float* f, const float* disp3,
                   const CharsInfo& ci, int degree, const float* q, float* out) {
@@ -1056,47 +893,29 @@ void interp_sweep(vreg_ctx ctx, const Slab& s, const float* f, const float* disp
   }
   const bool dist = ctx->nranks > 1;
   Ghosts gh;
-  if (dist && !use_tile())
-    gh = halo_exchange(ctx, s, f, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
   Timed t(ctx, T_SL, "sl_interp");
   const Geo g = geo_of(s);
-  const dim3 grid = sl_grid(s), block(BX, BY);
-  if (use_tile()) {
-    const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
-    const bool pipe = use_pipe(s, {f, disp3, q, out});
-    gather_tiles(ctx, s, f, ci.G, dist, gh, [&](TileZ zm, int nz) {
-      if (pipe) {
-        gather_pipe<0>(ctx, s, degree, dist, f, gh, tl.boxes, disp3, q, out, 0.f, 0, nullptr, zm,
-                       nz);
-        return;
-      }
-      SL_DISPATCH(degree, dist,
-                  (tile_kernel(k_gather_tile<DEG, DIST, 0>)<<<tile_grid_nz(s, nz), TILE_THREADS,
-                                                               tl.smem, ctx->stream>>>(
-                      g, src_of<DIST>(f, gh), tl.boxes, disp3, q, out, nullptr, nullptr, 0.f, 0,
-                      nullptr, zm)));
-    });
-  }
-  else if (use_quad(s))
+  const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
+  const bool pipe = use_pipe(s, {f, disp3, q, out});
+  gather_tiles(ctx, s, f, ci.G, dist, gh, [&](TileZ zm, int nz) {
+    if (pipe) {
+      gather_pipe<0>(ctx, s, degree, dist, f, gh, tl.boxes, disp3, q, out, 0.f, 0, nullptr, zm,
+                     nz);
+      return;
+    }
     SL_DISPATCH(degree, dist,
-                (k_interp_q<DEG, DIST><<<slq_grid(s), block, 0, ctx->stream>>>(
-                    g, src_of<DIST>(f, gh), disp3, q, out)));
-  else if (q)
-    SL_DISPATCH(degree, dist,
-                (k_interp_mul<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
-                    g, src_of<DIST>(f, gh), disp3, q, out)));
-  else
-    SL_DISPATCH(degree, dist,
-                (k_interp<DEG, DIST><<<grid, block, 0, ctx->stream>>>(g, src_of<DIST>(f, gh),
-                                                                      disp3, out)));
+                (tile_kernel(k_gather_tile<DEG, DIST, 0>)<<<tile_grid_nz(s, nz), TILE_THREADS,
+                                                             tl.smem, ctx->stream>>>(
+                    g, src_of<DIST>(f, gh), tl.boxes, disp3, q, out, nullptr, nullptr, 0.f, 0,
+                    nullptr, zm)));
+  });
 }
 
-// out = I^T z (out is overwritten)
-// out = I^T z (out is overwritten). Tile path: deterministic fixed point
-// (k_scatter_tile); zmax = device max|z| bits of this sweep's input (computed
-// here when null), next_max (optional) receives max|out| bits for a
-// following sweep. The per-point fallback paths (VREG_SL_TILE=0) use fp32
-// atomics.
+// out = I^T z (out is overwritten). Default: per-tile fixed point flushed
+// with fp32 L2 reductions (k_scatter_tile_fp). Deterministic mode: one
+// global fixed-point scale (k_scatter_tile); zmax = device max|z| bits of
+// this sweep's input (computed here when null), next_max (optional)
+// receives max|out| bits for a following sweep.
 void scatter_sweep(vreg_ctx ctx, const Slab& s, const float* z, const float* disp3,
                    const CharsInfo& ci, int degree, float* out, unsigned* zmax = nullptr,
                    unsigned* next_max = nullptr) {
@@ -1118,8 +937,7 @@ void scatter_sweep(vreg_ctx ctx, const Slab& s, const float* z, const float* dis
   if (dist) acc = ghost_accumulators(ctx, s, ci.G, "sl_gacc");
   Timed t(ctx, T_SL, "sl_scatter_sweep");
   const Geo g = geo_of(s);
-  const dim3 grid = sl_grid(s), block(BX, BY);
-  if (use_tile() && !ctx->deterministic) {
+  if (!ctx->deterministic) {
     VB_CUDA(cudaMemsetAsync(out, 0, N * sizeof(float), ctx->stream));
     const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
     scatter_tiles(ctx, s, acc, out, dist, [&](TileZ zm, int nz) {
@@ -1130,55 +948,37 @@ void scatter_sweep(vreg_ctx ctx, const Slab& s, const float* z, const float* dis
     });
     return;
   }
-  if (use_tile()) {
-    if (!zmax) {
-      zmax = static_cast<unsigned*>(workspace(ctx, "sc_zmax", 64));
-      VB_CUDA(cudaMemsetAsync(zmax, 0, sizeof(unsigned), ctx->stream));
-      k_maxabs_bits<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, z, zmax);
-      count_launch(ctx);
-      check_launch();
-    }
-    if (dist)  // one scale on every rank
-      VB_NCCL(ncclAllReduce(zmax, zmax, 1, ncclUint32, ncclMax, ctx->comm, ctx->stream));
-    float* I = static_cast<float*>(workspace(ctx, "sc_fixed", N * sizeof(float)));  // int32
-    VB_CUDA(cudaMemsetAsync(I, 0, N * sizeof(float), ctx->stream));
-    const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
-    scatter_tiles(
-        ctx, s, acc, I, dist,
-        [&](TileZ zm, int nz) {
-          SL_DISPATCH(degree, dist,
-                      (tile_kernel(k_scatter_tile<DEG, DIST>)<<<tile_grid_nz(s, nz), TILE_THREADS,
-                                                                tl.smem, ctx->stream>>>(
-                          g, dst_of<DIST>(I, acc), tl.boxes, disp3, z, zmax, zm)));
-        },
-        true);
-    if (s.n3 % 4 == 0) {  // packed pairs (fixed_add)
-      k_fixed_finish<<<blocks_for(N / 4, 256), 256, 0, ctx->stream>>>(
-          N / 4, reinterpret_cast<const longlong2*>(I), zmax, reinterpret_cast<float4*>(out),
-          next_max);
-    } else {
-      k_fixed_finish1<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(
-          N, reinterpret_cast<const int*>(I), zmax, out, next_max);
-    }
-    count_launch(ctx);
-    check_launch();
-    return;
-  }
-  VB_CUDA(cudaMemsetAsync(out, 0, N * sizeof(float), ctx->stream));
-  if (use_quad(s))
-    SL_DISPATCH(degree, dist,
-                (k_scatter_q<DEG, DIST><<<slq_grid(s), block, 0, ctx->stream>>>(
-                    g, dst_of<DIST>(out, acc), disp3, z)));
-  else
-    SL_DISPATCH(degree, dist,
-                (k_scatter<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
-                    g, dst_of<DIST>(out, acc), disp3, z)));
-  if (dist) halo_reverse_add(ctx, s, acc, out, "sl_gacc");
-  if (next_max) {
-    k_maxabs_bits<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, out, next_max);
+  if (!zmax) {
+    zmax = static_cast<unsigned*>(workspace(ctx, "sc_zmax", 64));
+    VB_CUDA(cudaMemsetAsync(zmax, 0, sizeof(unsigned), ctx->stream));
+    k_maxabs_bits<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, z, zmax);
     count_launch(ctx);
     check_launch();
   }
+  if (dist)  // one scale on every rank
+    VB_NCCL(ncclAllReduce(zmax, zmax, 1, ncclUint32, ncclMax, ctx->comm, ctx->stream));
+  float* I = static_cast<float*>(workspace(ctx, "sc_fixed", N * sizeof(float)));  // int32
+  VB_CUDA(cudaMemsetAsync(I, 0, N * sizeof(float), ctx->stream));
+  const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
+  scatter_tiles(
+      ctx, s, acc, I, dist,
+      [&](TileZ zm, int nz) {
+        SL_DISPATCH(degree, dist,
+                    (tile_kernel(k_scatter_tile<DEG, DIST>)<<<tile_grid_nz(s, nz), TILE_THREADS,
+                                                              tl.smem, ctx->stream>>>(
+                        g, dst_of<DIST>(I, acc), tl.boxes, disp3, z, zmax, zm)));
+      },
+      true);
+  if (s.n3 % 4 == 0) {  // packed pairs (fixed_add)
+    k_fixed_finish<<<blocks_for(N / 4, 256), 256, 0, ctx->stream>>>(
+        N / 4, reinterpret_cast<const longlong2*>(I), zmax, reinterpret_cast<float4*>(out),
+        next_max);
+  } else {
+    k_fixed_finish1<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(
+        N, reinterpret_cast<const int*>(I), zmax, out, next_max);
+  }
+  count_launch(ctx);
+  check_launch();
 }
 
 }  // namespace
@@ -1204,15 +1004,9 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
   const int nt = s.nt;
   const float half = float(0.5 * s.dt());
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
-  // tile path: all u_t in one streaming pass, steps then read one float each
-  const bool fused_u = use_tile() && !ci.identity && N % 4 == 0 && al16(vt3) && al16(grads);
-  // peer-memory steps: w_t in the arena (its first 2N floats), the
-  // neighbours read their ghost planes from it (sl_matvec_psi placed psi there)
-  const bool p2p = fused_u && in_arena(ctx, psi_out) && p2p_sweeps(ctx, s, ci);
-  float* w = p2p ? reinterpret_cast<float*>(p2p_data(ctx, size_t(nt + 3) * N * sizeof(float)))
-                 : static_cast<float*>(workspace(ctx, "inc_w", 2 * N * sizeof(float)));
-  // the neighbours finished reading my w slots in the previous solve
-  if (p2p && ctx->pdone) p2p_wait(ctx, P2P_DONE, ctx->pdone);
+  // all u_t in one streaming pass; the steps then read one float each
+  const bool fused_u = !ci.identity && N % 4 == 0 && al16(vt3) && al16(grads);
+  float* w = static_cast<float*>(workspace(ctx, "inc_w", 2 * N * sizeof(float)));
   float* u = fused_u ? static_cast<float*>(workspace(ctx, "inc_u", size_t(nt) * N * sizeof(float)))
                      : nullptr;
   {
@@ -1236,33 +1030,12 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
     float* wn = last ? psi_out : w + size_t((t + 1) & 1) * N;
     float* mo = mt_all ? mt_all + size_t(t + 1) * N : nullptr;
     Ghosts gh;
-    if (dist && !use_tile())
-      gh = halo_exchange(ctx, s, wt, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
     Timed tm(ctx, T_SL, "sl_inc_step");
-    if (p2p) {
-      const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
-      const uint64_t ready = p2p_seq(ctx);
-      p2p_signal(ctx, P2P_READY, ready);            // my w_t is complete
-      if (t > 0 && !last) p2p_wait(ctx, P2P_DONE, ctx->pdone);  // wn's slot held w_{t-1}
-      gh.G = ci.G;
-      gh.lo = peer_plane(ctx, wt, false, size_t(s.n1l - ci.G) * s.plane());
-      gh.hi = peer_plane(ctx, wt, true, 0);
-      const LayerSplit ls = layer_split(s, ci.G);
-      auto launch = [&](TileZ zm, int nz) {
-        SL_DISPATCH(degree, true,
-                    (tile_kernel(k_gather_tile<DEG, DIST, 2>)<<<tile_grid_nz(s, nz), TILE_THREADS,
-                                                                 tl.smem, ctx->stream>>>(
-                        g, src_of<DIST>(wt, gh), tl.boxes, disp3, u + size_t(t) * N, wn, nullptr,
-                        nullptr, half, last ? 1 : 0, mo, zm)));
-      };
-      if (ls.on) launch(TileZ{ls.zb, 1 << 30, 0}, ls.ntz - 2 * ls.zb);  // interior first
-      p2p_wait(ctx, P2P_READY, ready);
-      if (ls.on)
-        launch(TileZ{0, ls.zb, ls.ntz - ls.zb}, 2 * ls.zb);
-      else
-        launch(kAllLayers, ls.ntz);
-      ctx->pdone = p2p_seq(ctx);
-      p2p_signal(ctx, P2P_DONE, ctx->pdone);        // done reading the neighbours' w_t
+    if (ci.identity) {  // identity characteristics: pointwise step
+      SL_DISPATCH(degree, dist,
+                  (k_inc_step<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
+                      g, src_of<DIST>(wt, gh), disp3, 1, vt3, grads + size_t(t + 1) * 3 * N,
+                      half, last ? 1 : 0, wn, mo)));
     } else if (fused_u) {
       const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
       const float* ut = u + size_t(t) * N;
@@ -1279,7 +1052,7 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
                         g, src_of<DIST>(wt, gh), tl.boxes, disp3, u + size_t(t) * N, wn, nullptr,
                         nullptr, half, last ? 1 : 0, mo, zm)));
       });
-    } else if (use_tile() && !ci.identity) {
+    } else {
       const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
       gather_tiles(ctx, s, wt, ci.G, dist, gh, [&](TileZ zm, int nz) {
         SL_DISPATCH(degree, dist,
@@ -1289,16 +1062,6 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
                         grads + size_t(t + 1) * 3 * N, half, last ? 1 : 0, mo, zm)));
       });
     }
-    else if (use_quad(s))
-      SL_DISPATCH(degree, dist,
-                  (k_inc_step_q<DEG, DIST><<<slq_grid(s), block, 0, ctx->stream>>>(
-                      g, src_of<DIST>(wt, gh), disp3, ci.identity ? 1 : 0, vt3,
-                      grads + size_t(t + 1) * 3 * N, half, last ? 1 : 0, wn, mo)));
-    else
-    SL_DISPATCH(degree, dist,
-                (k_inc_step<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
-                    g, src_of<DIST>(wt, gh), disp3, ci.identity ? 1 : 0, vt3,
-                    grads + size_t(t + 1) * 3 * N, half, last ? 1 : 0, wn, mo)));
   }
 }
 
@@ -1310,7 +1073,7 @@ void sl_transpose_sweeps(vreg_ctx ctx, const Slab& s, const float* disp3, int fl
   const size_t N = s.local();
   // max|psi_t| bits per slice: each sweep's finish hands the next its scale
   unsigned* mx = nullptr;
-  if (ctx->deterministic && use_tile() && !ci.identity) {
+  if (ctx->deterministic && !ci.identity) {
     mx = static_cast<unsigned*>(workspace(ctx, "sc_chain", size_t(s.nt + 1) * sizeof(unsigned)));
     VB_CUDA(cudaMemsetAsync(mx, 0, size_t(s.nt + 1) * sizeof(unsigned), ctx->stream));
     k_maxabs_bits<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, psi + size_t(s.nt) * N,
@@ -1318,57 +1081,18 @@ void sl_transpose_sweeps(vreg_ctx ctx, const Slab& s, const float* disp3, int fl
     count_launch(ctx);
     check_launch();
   }
-  if (in_arena(ctx, psi) && p2p_sweeps(ctx, s, ci)) {
-    // each sweep: zero my slice, handshake, boundary tiles add straight into
-    // the neighbours' slices, interior tiles, then wait for their adds
-    const Geo g = geo_of(s);
-    const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
-    const LayerSplit ls = layer_split(s, ci.G);
-    for (int t = s.nt; t > 0; --t) {
-      Timed tm(ctx, T_SL, "sl_scatter_sweep");
-      const float* z = psi + size_t(t) * N;
-      float* out = psi + size_t(t - 1) * N;
-      VB_CUDA(cudaMemsetAsync(out, 0, N * sizeof(float), ctx->stream));
-      const uint64_t zeroed = p2p_seq(ctx);
-      p2p_signal(ctx, P2P_ZEROED, zeroed);
-      GhostAcc acc;
-      acc.G = ci.G;
-      acc.lo = peer_plane(ctx, out, false, size_t(s.n1l - ci.G) * s.plane());
-      acc.hi = peer_plane(ctx, out, true, 0);
-      auto launch = [&](TileZ zm, int nz) {
-        SL_DISPATCH(degree, true,
-                    (tile_kernel(k_scatter_tile_fp<DEG, DIST>)<<<tile_grid_nz(s, nz),
-                                                                 TILE_THREADS, tl.smem,
-                                                                 ctx->stream>>>(
-                        g, dst_of<DIST>(out, acc), tl.boxes, disp3, z, zm)));
-      };
-      p2p_wait(ctx, P2P_ZEROED, zeroed);
-      const uint64_t added = p2p_seq(ctx);
-      if (ls.on) {
-        launch(TileZ{0, ls.zb, ls.ntz - ls.zb}, 2 * ls.zb);
-        p2p_signal(ctx, P2P_ADDED, added);
-        launch(TileZ{ls.zb, 1 << 30, 0}, ls.ntz - 2 * ls.zb);
-      } else {
-        launch(kAllLayers, ls.ntz);
-        p2p_signal(ctx, P2P_ADDED, added);
-      }
-      p2p_wait(ctx, P2P_ADDED, added);
-    }
-    return;
-  }
   for (int t = s.nt; t > 0; --t)
     scatter_sweep(ctx, s, psi + size_t(t) * N, disp3, ci, degree, psi + size_t(t - 1) * N,
                   mx ? mx + t : nullptr, mx && t > 1 ? mx + t - 1 : nullptr);
 }
 
-// psi buffer ((nt+1) slices) of a GN matvec: the peer arena when the fused
-// peer-memory sweeps apply, else a workspace.
+// psi buffer ((nt+1) slices) of a GN matvec
 float* sl_matvec_psi(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int degree) {
-  const size_t N = s.local();
-  const CharsInfo ci = chars_info(ctx, s, disp3, flags, degree);
-  if (p2p_sweeps(ctx, s, ci))
-    return reinterpret_cast<float*>(p2p_data(ctx, size_t(s.nt + 3) * N * sizeof(float))) + 2 * N;
-  return static_cast<float*>(workspace(ctx, "mv_psi", size_t(s.nt + 1) * N * sizeof(float)));
+  (void)disp3;
+  (void)flags;
+  (void)degree;
+  return static_cast<float*>(
+      workspace(ctx, "mv_psi", size_t(s.nt + 1) * s.local() * sizeof(float)));
 }
 
 void sl_assemble(vreg_ctx ctx, const Slab& s, int descending, const float* sl,
@@ -1411,30 +1135,22 @@ int sl_characteristics(vreg_ctx ctx, const Slab& s, const float* v3, int degree,
   }
   Timed t(ctx, T_SL, "sl_characteristics");
   const Geo g = geo_of(s);
-  const dim3 grid = sl_grid(s), block(BX, BY);
   const float m1 = float(-dt / s.h(0)), m2 = float(-dt / s.h(1)), m3 = float(-dt / s.h(2));
   const float c1 = float(-0.5 * dt / s.h(0)), c2 = float(-0.5 * dt / s.h(1)),
               c3 = float(-0.5 * dt / s.h(2));
-  if (use_tile()) {
-    // box bound from max|v| (the midpoint floors spread by <= 2 floor(dt vmax / h) + 1)
-    int ext[3];
-    const int T[3] = {TT1, TT2, TT3};
-    for (int a = 0; a < 3; ++a)
-      ext[a] = T[a] + (degree == 3 ? 3 : 1) + 2 * int(std::floor(dt * vmax / s.h(a))) + 2;
-    ext[2] = ((ext[2] + 3 + 3) / 4) * 4;
-    const int words = std::min(BOX_CAP, ext[0] * ext[1] * BOX_PITCH);
-    const size_t smem = size_t(words) * sizeof(float);
-    SL_DISPATCH(degree, dist,
-                (tile_kernel(k_chars_tile<DEG, DIST>)<<<tile_grid(s), TILE_THREADS, smem,
-                                                        ctx->stream>>>(
-                    g, src_of<DIST>(v3, g1), src_of<DIST>(v3 + N, g2),
-                    src_of<DIST>(v3 + 2 * N, g3), v3, m1, m2, m3, c1, c2, c3, words, disp3)));
-    return 0;
-  }
+  // box bound from max|v| (the midpoint floors spread by <= 2 floor(dt vmax / h) + 1)
+  int ext[3];
+  const int T[3] = {TT1, TT2, TT3};
+  for (int a = 0; a < 3; ++a)
+    ext[a] = T[a] + (degree == 3 ? 3 : 1) + 2 * int(std::floor(dt * vmax / s.h(a))) + 2;
+  ext[2] = ((ext[2] + 3 + 3) / 4) * 4;
+  const int words = std::min(BOX_CAP, ext[0] * ext[1] * BOX_PITCH);
+  const size_t smem = size_t(words) * sizeof(float);
   SL_DISPATCH(degree, dist,
-              (k_characteristics<DEG, DIST><<<grid, block, 0, ctx->stream>>>(
+              (tile_kernel(k_chars_tile<DEG, DIST>)<<<tile_grid(s), TILE_THREADS, smem,
+                                                      ctx->stream>>>(
                   g, src_of<DIST>(v3, g1), src_of<DIST>(v3 + N, g2),
-                  src_of<DIST>(v3 + 2 * N, g3), v3, m1, m2, m3, c1, c2, c3, disp3)));
+                  src_of<DIST>(v3 + 2 * N, g3), v3, m1, m2, m3, c1, c2, c3, words, disp3)));
   return 0;
 }
 
@@ -1449,7 +1165,7 @@ void sl_source_factor(vreg_ctx ctx, const Slab& s, const float* d, const float* 
   const Geo g = geo_of(s);
   const dim3 grid = sl_grid(s), block(BX, BY);
   const float half = float(0.5 * s.dt());
-  if (use_tile() && !ci.identity) {
+  if (!ci.identity) {
     const TileLaunch tl = tile_table(ctx, s, disp_bwd3, degree, false);
     if (use_pipe(s, {d, disp_bwd3, q})) {
       gather_pipe<3>(ctx, s, degree, dist, d, gh, tl.boxes, disp_bwd3, d, q, half, 0, nullptr,
@@ -1479,7 +1195,7 @@ int vreg_characteristics(vreg_ctx ctx, const vreg_grid* g, const float* v3, int 
   return guard([&] {
     Slab s = slab_of(ctx, g);
     int ident = sl_characteristics(ctx, s, v3, degree, disp3);
-    if (!ident && use_tile()) tile_table(ctx, s, disp3, degree, true);
+    if (!ident) tile_table(ctx, s, disp3, degree, true);
     int flags = ident;
     if (ctx->nranks > 1 && !ident) flags |= (sl_ghost_width(ctx, s, disp3, degree) + 1) << 8;
     if (identity) *identity = flags;

@@ -1,6 +1,10 @@
-// Persistent, warp-specialised SL sweeps fed by the Tensor Memory
-// Accelerator (the gather of interp.cpp:70-108 and its exact transpose
-// interp.cpp:92-123, fused into the transport steps of transport.hpp).
+// Persistent, warp-specialised SL gather sweeps fed by the Tensor Memory
+// Accelerator (the gather of interp.cpp:70-108, fused into the transport
+// steps of transport.hpp). The transpose sweeps stay on the 3-CTA/SM tile
+// kernels of sl_tile.cuh: a pipelined variant (accumulate in the consumer
+// warps, flush by the producer group) measured 332 us against 267 us at
+// 256^3 -- one CTA per SM serialises the atomic and flush phases that three
+// independent CTAs overlap.
 //
 // One CTA per SM walks the 4 x 16 x 32 departure-point tiles of a launch
 // (tile = blockIdx.x + n * gridDim.x, x3 fastest, so co-resident CTAs work on
@@ -117,18 +121,18 @@ struct PipeTiles {
 // n3 % 4 == 0, k_tile_boxes), so each instruction moves whole lines.
 // Completion: thread 0's expect_tx arrival (TMA bytes) plus one
 // cp.async.mbarrier.arrive.noinc per producer thread.
-template <bool DIST, class Field>
+template <bool DIST, class Field, class RowT>
 __device__ __forceinline__ void pipe_produce(const Geo& g, const Field& src, const int* boxes,
                                              const CUtensorMap* tmD, const CUtensorMap* tmA,
                                              bool load_box, const PipeTiles& pt, const TileZ& zm,
-                                             int tile, float* st, PipeHdr* hdr,
-                                             const float** rows, uint64_t* full) {
+                                             int tile, float* st, PipeHdr* hdr, RowT** rows,
+                                             uint64_t* full) {
   const int t = threadIdx.x - PIPE_CONS;
   int layer, y, x;
   pt.coords(tile, zm, layer, y, x);
   const TileBox b = load_tile_box(boxes, (layer * pt.ty + y) * pt.tx + x);
-  const bool fits = load_box && b.ext[0] > 0 && b.ext[2] <= PIPE_P3 &&
-                    b.ext[0] * b.ext[1] <= PIPE_BOX_ROWS;
+  const bool fits =
+      load_box && b.ext[0] > 0 && b.ext[2] <= PIPE_P3 && b.ext[0] * b.ext[1] <= PIPE_BOX_ROWS;
   if (t == 0) {
     PipeHdr h;
     for (int a = 0; a < 3; ++a) {
@@ -165,6 +169,7 @@ __device__ __forceinline__ void pipe_produce(const Geo& g, const Field& src, con
       for (int r = t >> 4; r < nr; r += PIPE_PROD / 16) cp_async16(sb + r * PIPE_P3, rows[r] + col);
     }
   }
+  // arrives once this thread's box chunks have landed
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(full))
                : "memory");
 }

@@ -13,9 +13,10 @@
 // scatter: contributions accumulate in a shared-memory box in 32-bit fixed
 //          point (native ATOMS.ADD; fp32 smem atomics are a CAS loop on
 //          sm_100a, ~4x slower, tools/smem_atomic_bench.cu) with a per-tile
-//          power-of-two scale S = 2^(27-e), max|z_tile| < 2^e, so each
-//          contribution is exact to 2^-28 max|z| and a cell absorbs > 8
-//          max|z| without overflow. Each contribution is rounded by one
+//          power-of-two scale S = 2^(26-e), max|z_tile| < 2^e, so each
+//          contribution is exact to 2^-27 max|z| and a cell absorbs 32
+//          max|z| without overflow; tiles with non-finite z use fp32
+//          global atomics (NaN / Inf propagate). Each contribution is rounded by one
 //          DFMA against 1.5 * 2^52 (F2I is quarter-rate XU and was the
 //          binding pipe). The box is flushed once with float4 REDs:
 //          ~3 L2 reductions per point instead of 64 (the L2 RED path is
