@@ -41,7 +41,8 @@ typedef struct {
   int nt;
   double armijo_c, armijo_shrink;
   int armijo_max_trials, h0_inner_cap;
-  int pcg_fp64; /* B200: PCG iterates in fp64 around the fp32 operator (default 1) */
+  int pcg_fp64;  /* B200: PCG iterates in fp64 around the fp32 operator (default 1) */
+  int reg_order; /* B200: 1 = H1 (reference, default), 2 = H2 (symbol |k|^4) */
 } vreg_config;
 
 typedef struct vreg_solver_s* vreg_solver;

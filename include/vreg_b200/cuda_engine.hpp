@@ -348,6 +348,32 @@ class CudaEngine {
     out.from_host(f.v.data());
     return out;
   }
+  // Engine fields -> host fields of the whole grid (slab gather over the
+  // ranks), engine.hpp:64,66. HostScalar / HostVector are any types with a
+  // Grid3 constructor and `v` / comp(c).v storage (the reference's
+  // ScalarField / VectorField).
+  template <class HostScalar>
+  HostScalar to_global(const Field& f) const {
+    HostScalar out(grid_);
+    const std::vector<double> h = f.to_host();
+    for (size_t i = 0; i < h.size(); ++i) out.v[i] = h[i];
+    return out;
+  }
+  template <class HostVector>
+  HostVector to_global_v(const VField& f) const {
+    HostVector out(grid_);
+    const std::vector<double> h = f.to_host();
+    const size_t N = size_t(grid_.points());
+    for (int c = 0; c < 3; ++c)
+      for (size_t i = 0; i < N; ++i) out.comp(c).v[i] = h[size_t(c) * N + i];
+    return out;
+  }
+#ifdef VREG_B200_WITH_REFERENCE
+  vreg::ScalarField to_global(const Field& f) const { return to_global<vreg::ScalarField>(f); }
+  vreg::VectorField to_global_v(const VField& f) const {
+    return to_global_v<vreg::VectorField>(f);
+  }
+#endif
   template <class HostVector>
   VField from_global_v(const HostVector& v) const {
     const size_t N = size_t(grid_.points());

@@ -55,6 +55,9 @@ struct RegistrationConfig {
   // B200 extension: PCG iterates in fp64 (x, r, p) around the fp32 operator
   // (SURVEY §7 hard part 3); off = fp32 vectors rounded every update
   bool pcg_fp64 = true;
+  // B200 extension: regularisation order, 1 = H1 (the reference), 2 = H2
+  // (beta/2 |Delta v|^2, symbol |k|^4)
+  int reg_order = 1;
 
   bool fixed() const { return fixed_gn > 0; }
 
@@ -67,10 +70,13 @@ struct RegistrationConfig {
     need(precond == PrecondKind::InvA || (eps_h0 > 0 && eps_h0 < 1),
          "eps_h0 must lie in (0,1)");
     need(gamma_div >= 0, "gamma_div must be >= 0");
-    need(interp_degree == 1 || interp_degree == 3, "interp_degree must be 1 or 3");
+    // 1 trilinear, 3 cubic Lagrange (reference); 4 cubic B-spline (B200)
+    need(interp_degree == 1 || interp_degree == 3 || interp_degree == 4,
+         "interp_degree must be 1, 3 or 4");
     need(nt >= 1, "nt must be >= 1");
     need(max_gn >= 1 && max_pcg >= 1, "iteration caps must be >= 1");
     need((fixed_gn > 0) == (fixed_pcg > 0), "fixed_gn and fixed_pcg go together");
+    need(reg_order == 1 || reg_order == 2, "reg_order must be 1 (H1) or 2 (H2)");
   }
 };
 

@@ -51,6 +51,11 @@ typedef struct {
 
 typedef struct vreg_ctx_s* vreg_ctx;
 
+/* Interpolation `degree` arguments: 1 trilinear, 3 cubic Lagrange (the
+ * reference's two, interp.cpp:26-35), VREG_INTERP_BSPLINE3 cubic B-spline
+ * on prefiltered coefficients (B200 extension named by the north star). */
+#define VREG_INTERP_BSPLINE3 4
+
 /* One context per GPU (per rank). EngineState analogue (engine.hpp:14-19):
  * stream, FFT plan cache keyed by grid, reduction scratch, memory pool,
  * kernel timers, NCCL communicator. */
@@ -76,6 +81,12 @@ int vreg_halo_chunks(int n1l, int G, int cap, int* d, int* c, long long* lo, lon
  * independent of the GPU count, ~10% slower matvec. Default off (fp32 L2
  * reductions, run-to-run differences in the last bits); env VREG_DETERMINISTIC=1. */
 int vreg_ctx_set_deterministic(vreg_ctx ctx, int on);
+/* Order of the regularisation operator A used by regop / inv_regop /
+ * seminorm / h0_matvec / the GN matvec: 1 = H1, symbol |k|^2 (the
+ * reference, spectral.cpp:61-63; default), 2 = H2, symbol |k|^4 (B200
+ * extension named by the north star; no reference oracle -- analytic
+ * single-mode checks in tests/test_gpu_kernels.py). */
+int vreg_ctx_set_reg_order(vreg_ctx ctx, int order);
 /* The stream all calls on ctx are ordered on (cudaStream_t). */
 int vreg_ctx_get_stream(vreg_ctx ctx, void** stream);
 int vreg_ctx_set_stream(vreg_ctx ctx, void* cuda_stream);

@@ -34,6 +34,7 @@ _SIGS = {
     "vreg_ctx_set_stream": (I, [VP, VP]),
     "vreg_ctx_get_stream": (I, [VP, C.POINTER(VP)]),
     "vreg_ctx_set_deterministic": (I, [VP, I]),
+    "vreg_ctx_set_reg_order": (I, [VP, I]),
     "vreg_ctx_reserve": (I, [VP, C.c_size_t]),
     "vreg_halo_chunks": (I, [I, I, I, C.POINTER(I), C.POINTER(I), C.POINTER(C.c_longlong),
                              C.POINTER(C.c_longlong)]),

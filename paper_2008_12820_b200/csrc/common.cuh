@@ -126,6 +126,9 @@ struct vreg_ctx_s {
   // transpose sweeps in exact fixed point (bitwise reproducible, independent
   // of the GPU count) instead of fp32 L2 reductions (VREG_DETERMINISTIC=1)
   bool deterministic = false;
+  // regularisation order of the spectral operators: 1 = H1 (symbol |k|^2,
+  // the reference's spectral.cpp:61-63), 2 = H2 (|k|^4, B200 extension)
+  int reg_order = 1;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;
   // regulariser x2-slab transposes by copy engine into the peers' buffers

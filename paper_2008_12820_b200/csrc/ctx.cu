@@ -312,6 +312,13 @@ int vreg_ctx_set_deterministic(vreg_ctx ctx, int on) {
   return guard([&] { ctx->deterministic = on != 0; });
 }
 
+int vreg_ctx_set_reg_order(vreg_ctx ctx, int order) {
+  return guard([&] {
+    require(order == 1 || order == 2, VREG_EPARAM, "regularization order must be 1 (H1) or 2 (H2)");
+    ctx->reg_order = order;
+  });
+}
+
 int vreg_ctx_get_stream(vreg_ctx ctx, void** s) {
   return guard([&] {
     require(s != nullptr, VREG_EPARAM, "null argument");

@@ -271,7 +271,7 @@ void halo_reverse_add(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, float* o
 
 int sl_ghost_width(vreg_ctx ctx, const Slab& s, const float* disp1, int degree) {
   const double m = reduce(ctx, s, 1, disp1, disp1, true);
-  const int G = int(std::floor(m)) + (degree == 3 ? 3 : 2);
+  const int G = int(std::floor(m)) + (degree != 1 ? 3 : 2);
   // wider than the slab: multi-rank (wide) halos, see halo_chunks
   require(G <= 2 * s.n1, VREG_ECONFIG, "displacement exceeds twice the domain");
   return G;

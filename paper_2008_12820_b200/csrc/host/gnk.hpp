@@ -349,7 +349,7 @@ class DevicePrecond {
   // One stand-alone apply (not inside a captured solve): the whole apply is
   // a cached graph per (refresh, eps_k), replayed on fixed buffers.
   void apply_once(const float* r, float* z, Real eps_k) {
-    if (kind_ == PrecondKind::InvA || !graph_ok()) {
+    if (kind_ == PrecondKind::InvA || !graph_ok() || eng_->workers() > 1) {
       apply(r, z, eps_k);
       return;
     }
@@ -449,7 +449,8 @@ class DevicePrecond {
   }
   vb::Krylov& inner(CudaEngine& e, const DVField&) {
     auto& k = e.is_coarse() ? kc_ : kf_;
-    if (!k) k = std::make_unique<vb::Krylov>(e.ctx(), slab_for(e.ctx(), e.grid()));
+    // fp32 iterates: the inner tolerance is eps_h0 eps_k (~1e-4)
+    if (!k) k = std::make_unique<vb::Krylov>(e.ctx(), slab_for(e.ctx(), e.grid()), false);
     return *k;
   }
   vb::KrylovOp op_h0(CudaEngine& e, const DVField& gm) {
@@ -492,8 +493,9 @@ class OuterPcg {
   OuterPcg(CudaEngine& eng) : eng_(&eng) {}
   PcgOutcome solve(Transport& tr, DevicePrecond& pc, Real beta, const RegistrationConfig& cfg,
                    const DVField& g, Real eps_k, DVField& dv) {
-    if (!kr_) kr_ = std::make_unique<vb::Krylov>(eng_->ctx(), slab_for(eng_->ctx(), eng_->grid()));
-    kr_->set_fp32_iterates(!cfg.pcg_fp64);
+    if (!kr_ || kr_->fp64() != cfg.pcg_fp64)
+      kr_ = std::make_unique<vb::Krylov>(eng_->ctx(), slab_for(eng_->ctx(), eng_->grid()),
+                                         cfg.pcg_fp64);
     DVField rhs = eng_->make_vfield();
     axpy(Real(-1), g, rhs);
     const bool fixed = cfg.fixed();

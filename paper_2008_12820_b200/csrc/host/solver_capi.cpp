@@ -106,6 +106,7 @@ RegistrationConfig from_c(const vreg_config* c) {
   r.armijo_max_trials = c->armijo_max_trials;
   r.h0_inner_cap = c->h0_inner_cap;
   r.pcg_fp64 = c->pcg_fp64 != 0;
+  r.reg_order = c->reg_order;
   return r;
 }
 
@@ -122,6 +123,14 @@ void dump_counters(const KernelCounters& k, uint64_t* o) {
 void require_lin(const vreg_solver_s* s) {
   if (!s->lin) throw config_error("solver not linearised (call vreg_solver_linearize)");
 }
+
+// The context's regularisation order follows the solver's config for the
+// duration of a call (the context may serve several solvers).
+struct OrderScope {
+  vreg_ctx ctx;
+  OrderScope(const vreg_solver_s* s) : ctx(s->eng.ctx()) { check(vreg_ctx_set_reg_order(ctx, s->cfg.reg_order)); }
+  ~OrderScope() { vreg_ctx_set_reg_order(ctx, 1); }
+};
 
 }  // namespace
 
@@ -150,6 +159,7 @@ void vreg_config_default(vreg_config* c) {
   c->armijo_max_trials = r.armijo_max_trials;
   c->h0_inner_cap = r.h0_inner_cap;
   c->pcg_fp64 = r.pcg_fp64;
+  c->reg_order = r.reg_order;
 }
 
 int vreg_solver_create(vreg_ctx ctx, const vreg_grid* g, const vreg_config* cfg,
@@ -211,6 +221,7 @@ int vreg_solver_images(vreg_solver s, float* m0, float* m1) {
 
 int vreg_solver_linearize(vreg_solver s, const float* v3, double beta) {
   return guarded([&] {
+    OrderScope order(s);
     if (beta <= 0) throw parameter_error("beta must be > 0");
     CudaEngine& e = s->eng;
     DVField v = e.make_vfield();
@@ -263,6 +274,7 @@ bool direct_matvec(vreg_solver s, const float* vt3, float* out3) {
 
 int vreg_solver_matvec(vreg_solver s, const float* vt3, float* out3) {
   return guarded([&] {
+    OrderScope order(s);
     require_lin(s);
     if (direct_matvec(s, vt3, out3)) return;
     CudaEngine& e = s->eng;
@@ -273,6 +285,7 @@ int vreg_solver_matvec(vreg_solver s, const float* vt3, float* out3) {
 
 int vreg_solver_matvec_host(vreg_solver s, const float* vt3_host, float* out3_host) {
   return guarded([&] {
+    OrderScope order(s);
     require_lin(s);
     CudaEngine& e = s->eng;
     if (!s->io_in) {
@@ -297,6 +310,7 @@ void cuda_check(cudaError_t e) {
 
 int vreg_solver_matvec_host_async(vreg_solver s, const float* vt3_host, float* out3_host) {
   return guarded([&] {
+    OrderScope order(s);
     require_lin(s);
     CudaEngine& e = s->eng;
     void* mv = nullptr;
@@ -348,6 +362,7 @@ int vreg_solver_wait(vreg_solver s) {
 int vreg_solver_precond(vreg_solver s, int kind, const float* r3, double eps_k, float* out3,
                         uint64_t stats4[4]) {
   return guarded([&] {
+    OrderScope order(s);
     require_lin(s);
     CudaEngine& e = s->eng;
     if (kind < 0 || kind > 2) throw parameter_error("preconditioner kind must be 0, 1 or 2");
@@ -372,6 +387,7 @@ int vreg_solver_precond(vreg_solver s, int kind, const float* r3, double eps_k, 
 
 int vreg_solver_register(vreg_solver s, float* v_out3, double rep16[16], uint64_t counters21[21]) {
   return guarded([&] {
+    OrderScope order(s);
     CudaEngine& e = s->eng;
     DVField v;
     SolverReport r = Registration(e, s->m0, s->m1, s->cfg).run(&v);

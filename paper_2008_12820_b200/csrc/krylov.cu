@@ -19,8 +19,6 @@ constexpr int KT = 256;  // threads of the partial-sum kernels
 
 // One CTA per (component, local plane, chunk); returns the CTA's fp64 sum of
 // f(i) over its chunk (thread 0 holds it).
-__device__ __forceinline__ double rnd(double v, bool f32) { return f32 ? double(float(v)) : v; }
-
 template <class F>
 __device__ __forceinline__ double chunk_sum(size_t plane, int n1l, int chunks, F f) {
   const int cta = blockIdx.x;
@@ -48,69 +46,76 @@ struct Geo3 {
   int n1l, chunks;
 };
 
+// Iterates of type T: double (the reference's Real) or float (fp32 storage;
+// the operator's fp32 copies then alias the iterates themselves).
+
 // r = b - (x0 ? q : 0), r32 = r, x = x0 ? x32 : 0; partial r.r
-__global__ void __launch_bounds__(KT) k_init(Geo3 g, bool f32, const float* __restrict__ b,
+template <class T>
+__global__ void __launch_bounds__(KT) k_init(Geo3 g, const float* __restrict__ b,
                                              const float* __restrict__ q,
-                                             const float* __restrict__ x32, double* __restrict__ x,
-                                             double* __restrict__ r, float* __restrict__ r32,
-                                             double* __restrict__ part) {
+                                             const float* __restrict__ x32, T* x, T* r,
+                                             float* r32, double* __restrict__ part) {
+  const bool copy = static_cast<void*>(r32) != static_cast<void*>(r);
   const double s = chunk_sum(g.plane, g.n1l, g.chunks, [&](size_t i) {
-    const double ri = rnd(double(b[i]) - (q ? double(q[i]) : 0.0), f32);
+    const T ri = T(double(b[i]) - (q ? double(q[i]) : 0.0));
     r[i] = ri;
-    r32[i] = float(ri);
-    x[i] = x32 ? double(x32[i]) : 0.0;
-    return ri * ri;
+    if (copy) r32[i] = float(ri);
+    x[i] = x32 ? T(x32[i]) : T(0);
+    return double(ri) * double(ri);
   });
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// partial a.b (a fp64, b fp32)
-__global__ void __launch_bounds__(KT) k_dot(Geo3 g, const double* __restrict__ a,
+// partial a.b (a an iterate, b fp32)
+template <class T>
+__global__ void __launch_bounds__(KT) k_dot(Geo3 g, const T* __restrict__ a,
                                             const float* __restrict__ b,
                                             double* __restrict__ part) {
-  const double s =
-      chunk_sum(g.plane, g.n1l, g.chunks, [&](size_t i) { return a[i] * double(b[i]); });
+  const double s = chunk_sum(g.plane, g.n1l, g.chunks,
+                             [&](size_t i) { return double(a[i]) * double(b[i]); });
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
 // p = z + beta p (p = z on the first iteration), p32 = p
+template <class T>
 __global__ void k_dir(size_t n, const KrylovState* __restrict__ st, const float* __restrict__ z,
-                      double* __restrict__ p, float* __restrict__ p32) {
+                      T* p, float* p32) {
   if (st->pad) return;
-  const bool f32 = st->round32 != 0;
+  const bool copy = static_cast<void*>(p32) != static_cast<void*>(p);
   const bool first = st->it == 0;
   const double beta = st->beta;
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const double v = rnd(first ? double(z[i]) : double(z[i]) + beta * p[i], f32);
+    const T v = T(first ? double(z[i]) : double(z[i]) + beta * double(p[i]));
     p[i] = v;
-    p32[i] = float(v);
+    if (copy) p32[i] = float(v);
   }
 }
 
 // x += alpha p, r -= alpha q, r32 = r (skipped after negative curvature); partial r.r
+template <class T>
 __global__ void __launch_bounds__(KT) k_step(Geo3 g, const KrylovState* __restrict__ st,
-                                             const double* __restrict__ p,
-                                             const float* __restrict__ q, double* __restrict__ x,
-                                             double* __restrict__ r, float* __restrict__ r32,
-                                             double* __restrict__ part) {
+                                             const T* __restrict__ p,
+                                             const float* __restrict__ q, T* __restrict__ x,
+                                             T* r, float* r32, double* __restrict__ part) {
   if (st->negcurv || st->pad) {
     if (threadIdx.x == 0) part[blockIdx.x] = 0.0;
     return;
   }
+  const bool copy = static_cast<void*>(r32) != static_cast<void*>(r);
   const double a = st->alpha;
-  const bool f32 = st->round32 != 0;
   const double s = chunk_sum(g.plane, g.n1l, g.chunks, [&](size_t i) {
-    x[i] = rnd(x[i] + a * p[i], f32);
-    const double ri = rnd(r[i] - a * double(q[i]), f32);
+    x[i] = T(double(x[i]) + a * double(p[i]));
+    const T ri = T(double(r[i]) - a * double(q[i]));
     r[i] = ri;
-    r32[i] = float(ri);
-    return ri * ri;
+    if (copy) r32[i] = float(ri);
+    return double(ri) * double(ri);
   });
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-__global__ void k_to_f32(size_t n, const double* __restrict__ x, float* __restrict__ y) {
+template <class T>
+__global__ void k_to_f32(size_t n, const T* __restrict__ x, float* __restrict__ y) {
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
     y[i] = float(x[i]);
@@ -202,10 +207,9 @@ __global__ void __launch_bounds__(KT) k_fold(int mode, int nranks, int n1l, int 
     cudaGraphSetConditional(cudaGraphConditionalHandle(cond), S.stop ? 0u : 1u);
 }
 
-__global__ void k_set_state(KrylovState* st, double tol, int max_it, int round32) {
+__global__ void k_set_state(KrylovState* st, double tol, int max_it) {
   st->tol = tol;
   st->max_it = max_it;
-  st->round32 = round32;
 }
 
 // acc[0] += iterations, acc[1] |= not converged
@@ -220,17 +224,23 @@ inline void cuda_ok(cudaError_t e, const char* what) {
 
 }  // namespace
 
-Krylov::Krylov(vreg_ctx ctx, const Slab& s) : ctx_(ctx), s_(s) {
+Krylov::Krylov(vreg_ctx ctx, const Slab& s, bool fp64) : ctx_(ctx), s_(s), fp64_(fp64) {
   chunks_ = chunks_per_plane(s);
   n3_ = 3 * s.local();
   require(s.n1 <= 1024, VREG_ECONFIG, "Krylov fold supports n1 <= 1024");
-  cuda_ok(cudaMallocAsync(&x_, n3_ * sizeof(double), ctx->stream), "krylov alloc");
-  cuda_ok(cudaMallocAsync(&r_, n3_ * sizeof(double), ctx->stream), "krylov alloc");
-  cuda_ok(cudaMallocAsync(&p_, n3_ * sizeof(double), ctx->stream), "krylov alloc");
+  const size_t es = fp64 ? sizeof(double) : sizeof(float);
+  cuda_ok(cudaMallocAsync(&x_, n3_ * es, ctx->stream), "krylov alloc");
+  cuda_ok(cudaMallocAsync(&r_, n3_ * es, ctx->stream), "krylov alloc");
+  cuda_ok(cudaMallocAsync(&p_, n3_ * es, ctx->stream), "krylov alloc");
   cuda_ok(cudaMallocAsync(&z32_, n3_ * sizeof(float), ctx->stream), "krylov alloc");
   cuda_ok(cudaMallocAsync(&q32_, n3_ * sizeof(float), ctx->stream), "krylov alloc");
-  cuda_ok(cudaMallocAsync(&p32_, n3_ * sizeof(float), ctx->stream), "krylov alloc");
-  cuda_ok(cudaMallocAsync(&r32_, n3_ * sizeof(float), ctx->stream), "krylov alloc");
+  if (fp64) {  // fp32 copies for the operator; fp32 iterates are their own copies
+    cuda_ok(cudaMallocAsync(&p32_, n3_ * sizeof(float), ctx->stream), "krylov alloc");
+    cuda_ok(cudaMallocAsync(&r32_, n3_ * sizeof(float), ctx->stream), "krylov alloc");
+  } else {
+    p32_ = static_cast<float*>(p_);
+    r32_ = static_cast<float*>(r_);
+  }
   const size_t np = size_t(3) * s.n1l * chunks_;
   cuda_ok(cudaMallocAsync(&part_, np * sizeof(double), ctx->stream), "krylov alloc");
   if (ctx->nranks > 1)
@@ -244,9 +254,9 @@ Krylov::Krylov(vreg_ctx ctx, const Slab& s) : ctx_(ctx), s_(s) {
 
 Krylov::~Krylov() {
   cudaStreamSynchronize(ctx_->stream);
-  for (void* q : {static_cast<void*>(x_), static_cast<void*>(r_), static_cast<void*>(p_),
-                  static_cast<void*>(z32_), static_cast<void*>(q32_), static_cast<void*>(p32_),
-                  static_cast<void*>(r32_), static_cast<void*>(part_),
+  if (!fp64_) p32_ = r32_ = nullptr;  // aliases of p_ and r_
+  for (void* q : {x_, r_, p_, static_cast<void*>(z32_), static_cast<void*>(q32_),
+                  static_cast<void*>(p32_), static_cast<void*>(r32_), static_cast<void*>(part_),
                   static_cast<void*>(part_all_), static_cast<void*>(st_),
                   static_cast<void*>(hist_)})
     if (q) cudaFree(q);
@@ -271,12 +281,18 @@ void Krylov::issue_fold(int mode, unsigned long long cond) {
 
 void Krylov::issue_init(const KrylovOp& A, const float* b, const float* x, bool x0, double tol,
                         int max_it) {
-  k_set_state<<<1, 1, 0, ctx_->stream>>>(st_, tol, max_it, fp32_ ? 1 : 0);
+  k_set_state<<<1, 1, 0, ctx_->stream>>>(st_, tol, max_it);
   if (x0) A(x, q32_);  // r = b - A x0 (precond.hpp:141 inner solves, x_is_zero = false)
   const Geo3 g{s_.plane(), s_.n1l, chunks_};
   const unsigned nb = unsigned(3 * s_.n1l * chunks_);
-  k_init<<<nb, KT, 0, ctx_->stream>>>(g, fp32_, b, x0 ? q32_ : nullptr, x0 ? x : nullptr, x_, r_, r32_,
-                                       part_);
+  const float* qq = x0 ? q32_ : nullptr;
+  const float* xx = x0 ? x : nullptr;
+  if (fp64_)
+    k_init<double><<<nb, KT, 0, ctx_->stream>>>(g, b, qq, xx, static_cast<double*>(x_),
+                                                static_cast<double*>(r_), r32_, part_);
+  else
+    k_init<float><<<nb, KT, 0, ctx_->stream>>>(g, b, qq, xx, static_cast<float*>(x_),
+                                               static_cast<float*>(r_), r32_, part_);
   count_launch(ctx_, 2);
   check_launch();
 }
@@ -285,24 +301,50 @@ void Krylov::issue_body(const KrylovOp& A, const KrylovOp& M, unsigned long long
   const Geo3 g{s_.plane(), s_.n1l, chunks_};
   const unsigned nb = unsigned(3 * s_.n1l * chunks_);
   M(r32_, z32_);
-  k_dot<<<nb, KT, 0, ctx_->stream>>>(g, r_, z32_, part_);
-  count_launch(ctx_);
+  dot(r_, z32_);
   issue_fold(F_RZ, 0);
-  k_dir<<<blocks_for(n3_, 256), 256, 0, ctx_->stream>>>(n3_, st_, z32_, p_, p32_);
+  if (fp64_)
+    k_dir<double><<<blocks_for(n3_, 256), 256, 0, ctx_->stream>>>(
+        n3_, st_, z32_, static_cast<double*>(p_), p32_);
+  else
+    k_dir<float><<<blocks_for(n3_, 256), 256, 0, ctx_->stream>>>(
+        n3_, st_, z32_, static_cast<float*>(p_), p32_);
   count_launch(ctx_);
   A(p32_, q32_);
-  k_dot<<<nb, KT, 0, ctx_->stream>>>(g, p_, q32_, part_);
-  count_launch(ctx_);
+  dot(p_, q32_);
   issue_fold(F_PQ, 0);
-  k_step<<<nb, KT, 0, ctx_->stream>>>(g, st_, p_, q32_, x_, r_, r32_, part_);
+  if (fp64_)
+    k_step<double><<<nb, KT, 0, ctx_->stream>>>(g, st_, static_cast<const double*>(p_), q32_,
+                                                static_cast<double*>(x_),
+                                                static_cast<double*>(r_), r32_, part_);
+  else
+    k_step<float><<<nb, KT, 0, ctx_->stream>>>(g, st_, static_cast<const float*>(p_), q32_,
+                                               static_cast<float*>(x_), static_cast<float*>(r_),
+                                               r32_, part_);
   count_launch(ctx_);
   check_launch();
   issue_fold(F_RR, cond);
 }
 
-void Krylov::issue_finish(float* x, unsigned long long* acc) {
-  k_to_f32<<<blocks_for(n3_, 256), 256, 0, ctx_->stream>>>(n3_, x_, x);
+// per-plane partials of <a, b32> (a an iterate)
+void Krylov::dot(const void* a, const float* b32) {
+  const Geo3 g{s_.plane(), s_.n1l, chunks_};
+  const unsigned nb = unsigned(3 * s_.n1l * chunks_);
+  if (fp64_)
+    k_dot<double><<<nb, KT, 0, ctx_->stream>>>(g, static_cast<const double*>(a), b32, part_);
+  else
+    k_dot<float><<<nb, KT, 0, ctx_->stream>>>(g, static_cast<const float*>(a), b32, part_);
   count_launch(ctx_);
+}
+
+void Krylov::issue_finish(float* x, unsigned long long* acc) {
+  if (fp64_) {
+    k_to_f32<double><<<blocks_for(n3_, 256), 256, 0, ctx_->stream>>>(
+        n3_, static_cast<const double*>(x_), x);
+    count_launch(ctx_);
+  } else {
+    VB_CUDA(cudaMemcpyAsync(x, x_, n3_ * sizeof(float), cudaMemcpyDeviceToDevice, ctx_->stream));
+  }
   if (acc) {
     k_accumulate<<<1, 1, 0, ctx_->stream>>>(st_, acc);
     count_launch(ctx_);
@@ -399,11 +441,15 @@ KrylovStats Krylov::read_stats() {
 
 KrylovStats Krylov::solve(const KrylovOp& A, const KrylovOp& M, const float* b, float* x,
                           double tol, int max_it, bool x0, unsigned long long* acc, bool graph) {
-  static const bool graphs_on = [] {
+  // graphs on one GPU; on several the loop runs eagerly (one 64-byte state
+  // read per iteration) unless VREG_PCG_GRAPH=1 -- NCCL collectives of two
+  // communicators (halo/fold and the regulariser's transposes) inside one
+  // captured body are not ordered across ranks
+  static const int graphs_env = [] {
     const char* e = std::getenv("VREG_PCG_GRAPH");
-    return !(e && e[0] == '0');
+    return e ? (e[0] == '0' ? 0 : 1) : -1;
   }();
-  graph = graph && graphs_on;
+  graph = graph && (graphs_env == 1 || (graphs_env == -1 && ctx_->nranks == 1));
   if (max_it + 1 > hist_cap_) {
     if (hist_) cuda_ok(cudaFreeAsync(hist_, ctx_->stream), "history free");
     hist_cap_ = max_it + 1;

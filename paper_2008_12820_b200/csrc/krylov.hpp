@@ -2,7 +2,8 @@
 // H0 inner solves of precond.hpp:104-162), re-designed for the GPU:
 //
 //  * the iterate x, residual r and direction p are fp64 device vectors (the
-//    reference's Real); the operator and the preconditioner are fp32 device
+//    reference's Real) -- fp32 for the inner H0 solves, whose tolerance is
+//    eps_h0 eps_k; the operator and the preconditioner are fp32 device
 //    callbacks, fed fp32 copies written by the fused update kernels;
 //  * every scalar (rho, pq, alpha, beta, |r|, the stopping state, the
 //    relative-residual history) lives in device memory: inner products are
@@ -32,7 +33,6 @@ namespace vb {
 struct KrylovState {
   double rho, pq, alpha, beta, rr, r0n, tol;
   int it, max_it, stop, conv, negcurv, pad;
-  int round32, pad2;  // round32: iterates rounded to fp32 after every update
 };
 
 struct KrylovStats {
@@ -48,7 +48,9 @@ using KrylovOp = std::function<void(const float* in3, float* out3)>;
 
 class Krylov {
  public:
-  Krylov(vreg_ctx ctx, const Slab& s);
+  // fp64: iterates x, r, p in fp64 (the reference's Real); false: fp32
+  // iterates (the operator then reads them in place)
+  Krylov(vreg_ctx ctx, const Slab& s, bool fp64 = true);
   ~Krylov();
   Krylov(const Krylov&) = delete;
   Krylov& operator=(const Krylov&) = delete;
@@ -65,9 +67,7 @@ class Krylov {
                     int max_it, bool x0, unsigned long long* acc = nullptr, bool graph = true);
 
   const Slab& slab() const { return s_; }
-  // fp32 iterates (x, r, p rounded to fp32 after every update) instead of
-  // fp64: the A/B switch for the precision study (RegistrationConfig::pcg_fp64)
-  void set_fp32_iterates(bool on) { fp32_ = on; }
+  bool fp64() const { return fp64_; }
 
  private:
   void issue_init(const KrylovOp& A, const float* b, const float* x, bool x0, double tol,
@@ -75,6 +75,7 @@ class Krylov {
   void issue_body(const KrylovOp& A, const KrylovOp& M, unsigned long long cond);
   void issue_fold(int mode, unsigned long long cond);
   void issue_finish(float* x, unsigned long long* acc);
+  void dot(const void* a, const float* b32);
   KrylovStats read_stats();
   void capture_loop(const KrylovOp& A, const KrylovOp& M, bool nested);
 
@@ -82,7 +83,8 @@ class Krylov {
   Slab s_;
   int chunks_;
   size_t n3_;  // 3 N
-  double *x_ = nullptr, *r_ = nullptr, *p_ = nullptr;
+  bool fp64_;
+  void *x_ = nullptr, *r_ = nullptr, *p_ = nullptr;
   float *z32_ = nullptr, *q32_ = nullptr, *p32_ = nullptr, *r32_ = nullptr;
   double *part_ = nullptr, *part_all_ = nullptr;
   KrylovState* st_ = nullptr;
@@ -90,7 +92,6 @@ class Krylov {
   int hist_cap_ = 0;
   KrylovState* h_st_ = nullptr;  // pinned
   cudaStream_t cap_stream_ = nullptr;
-  bool fp32_ = false;
 };
 
 }  // namespace vb

@@ -18,6 +18,8 @@
 
 namespace vb {
 
+void bspline_prefilter(vreg_ctx ctx, const Slab& s, int ncomp, const float* in, float* out);
+
 namespace {
 
 constexpr int BX = 32, BY = 8;
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_chars_tile(
     Geo g, SrcField<DIST> s1, SrcField<DIST> s2, SrcField<DIST> s3, const float* __restrict__ v,
     float m1, float m2, float m3, float c1, float c2, float c3, int box_cap_words,
     float* __restrict__ D) {
-  constexpr int NN = DEG + 1, O0 = DEG == 3 ? -1 : 0;
+  constexpr int NN = Basis<DEG>::NN, O0 = Basis<DEG>::O0;
   extern __shared__ __align__(16) float fbox[];
   __shared__ const float* rows[BOX_ROWS_MAX];
   __shared__ int smn[3], smx[3];
@@ -675,7 +677,7 @@ TileLaunch tile_table(vreg_ctx ctx, const Slab& s, const float* disp3, int degre
   auto build = [&](int* table) -> int {
     int* mw = table + 6 * ntiles;  // [0] largest box words, [1] misfit tiles
     VB_CUDA(cudaMemsetAsync(mw, 0, 2 * sizeof(int), ctx->stream));
-    if (degree == 3)
+    if (degree != 1)  // both cubic bases reach nodes -1..2
       k_tile_boxes<3><<<grid, TILE_THREADS, 0, ctx->stream>>>(g, disp3, table, mw);
     else
       k_tile_boxes<1><<<grid, TILE_THREADS, 0, ctx->stream>>>(g, disp3, table, mw);
@@ -810,13 +812,34 @@ DstField<DIST> dst_of(float* f, const GhostAcc& gh) {
 }
 
 inline void check_degree(int degree) {
-  require(degree == 1 || degree == 3, VREG_EPARAM, "interpolation degree must be 1 or 3");
+  require(degree == 1 || degree == 3 || degree == VREG_INTERP_BSPLINE3, VREG_EPARAM,
+          "interpolation degree must be 1, 3 or 4 (cubic B-spline)");
+}
+
+// Source of a gather: the field itself, or for the cubic B-spline its
+// prefiltered coefficients (in the workspace `slot`).
+inline const float* gather_source(vreg_ctx ctx, const Slab& s, int degree, const float* f,
+                                  const char* slot) {
+  if (degree != VREG_INTERP_BSPLINE3) return f;
+  float* c = static_cast<float*>(workspace(ctx, slot, s.local() * sizeof(float)));
+  bspline_prefilter(ctx, s, 1, f, c);
+  return c;
 }
 
 // Dispatch a kernel template over (degree, dist).
 #define SL_DISPATCH(degree, dist, LAUNCH)                 \
   do {                                                    \
-    if (degree == 3) {                                    \
+    if (degree == VREG_INTERP_BSPLINE3) {                 \
+      if (dist) {                                         \
+        constexpr int DEG = 4;                            \
+        constexpr bool DIST = true;                       \
+        LAUNCH;                                           \
+      } else {                                            \
+        constexpr int DEG = 4;                            \
+        constexpr bool DIST = false;                      \
+        LAUNCH;                                           \
+      }                                                   \
+    } else if (degree == 3) {                             \
       if (dist) {                                         \
         constexpr int DEG = 3;                            \
         constexpr bool DIST = true;                       \
@@ -893,6 +916,7 @@ void interp_sweep(vreg_ctx ctx, const Slab& s, const float* f, const float* disp
   }
   const bool dist = ctx->nranks > 1;
   Ghosts gh;
+  f = gather_source(ctx, s, degree, f, "bs_coef");
   Timed t(ctx, T_SL, "sl_interp");
   const Geo g = geo_of(s);
   const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
@@ -946,6 +970,8 @@ void scatter_sweep(vreg_ctx ctx, const Slab& s, const float* z, const float* dis
                                                                tl.smem, ctx->stream>>>(
                       g, dst_of<DIST>(out, acc), tl.boxes, disp3, z, zm)));
     });
+    // B-spline: I = B P (P the symmetric prefilter), so I^T = P B^T
+    if (degree == VREG_INTERP_BSPLINE3) bspline_prefilter(ctx, s, 1, out, out);
     return;
   }
   if (!zmax) {
@@ -979,6 +1005,7 @@ void scatter_sweep(vreg_ctx ctx, const Slab& s, const float* z, const float* dis
   }
   count_launch(ctx);
   check_launch();
+  if (degree == VREG_INTERP_BSPLINE3) bspline_prefilter(ctx, s, 1, out, out);
 }
 
 }  // namespace
@@ -1030,6 +1057,8 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
     float* wn = last ? psi_out : w + size_t((t + 1) & 1) * N;
     float* mo = mt_all ? mt_all + size_t(t + 1) * N : nullptr;
     Ghosts gh;
+    // B-spline: the step gathers the coefficients of w_t
+    const float* src = ci.identity ? wt : gather_source(ctx, s, degree, wt, "bs_w");
     Timed tm(ctx, T_SL, "sl_inc_step");
     if (ci.identity) {  // identity characteristics: pointwise step
       SL_DISPATCH(degree, dist,
@@ -1039,26 +1068,26 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
     } else if (fused_u) {
       const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
       const float* ut = u + size_t(t) * N;
-      const bool pipe = use_pipe(s, {wt, disp3, ut, wn, mo});
-      gather_tiles(ctx, s, wt, ci.G, dist, gh, [&](TileZ zm, int nz) {
+      const bool pipe = use_pipe(s, {src, disp3, ut, wn, mo});
+      gather_tiles(ctx, s, src, ci.G, dist, gh, [&](TileZ zm, int nz) {
         if (pipe) {
-          gather_pipe<2>(ctx, s, degree, dist, wt, gh, tl.boxes, disp3, ut, wn, half,
+          gather_pipe<2>(ctx, s, degree, dist, src, gh, tl.boxes, disp3, ut, wn, half,
                          last ? 1 : 0, mo, zm, nz);
           return;
         }
         SL_DISPATCH(degree, dist,
                     (tile_kernel(k_gather_tile<DEG, DIST, 2>)<<<tile_grid_nz(s, nz), TILE_THREADS,
                                                                  tl.smem, ctx->stream>>>(
-                        g, src_of<DIST>(wt, gh), tl.boxes, disp3, u + size_t(t) * N, wn, nullptr,
+                        g, src_of<DIST>(src, gh), tl.boxes, disp3, u + size_t(t) * N, wn, nullptr,
                         nullptr, half, last ? 1 : 0, mo, zm)));
       });
     } else {
       const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
-      gather_tiles(ctx, s, wt, ci.G, dist, gh, [&](TileZ zm, int nz) {
+      gather_tiles(ctx, s, src, ci.G, dist, gh, [&](TileZ zm, int nz) {
         SL_DISPATCH(degree, dist,
                     (tile_kernel(k_gather_tile<DEG, DIST, 1>)<<<tile_grid_nz(s, nz), TILE_THREADS,
                                                                  tl.smem, ctx->stream>>>(
-                        g, src_of<DIST>(wt, gh), tl.boxes, disp3, nullptr, wn, vt3,
+                        g, src_of<DIST>(src, gh), tl.boxes, disp3, nullptr, wn, vt3,
                         grads + size_t(t + 1) * 3 * N, half, last ? 1 : 0, mo, zm)));
       });
     }
@@ -1073,7 +1102,9 @@ void sl_transpose_sweeps(vreg_ctx ctx, const Slab& s, const float* disp3, int fl
   const size_t N = s.local();
   // max|psi_t| bits per slice: each sweep's finish hands the next its scale
   unsigned* mx = nullptr;
-  if (ctx->deterministic && !ci.identity) {
+  // (the B-spline prefilter after each sweep changes max|psi|: those sweeps
+  // measure their own input)
+  if (ctx->deterministic && !ci.identity && degree != VREG_INTERP_BSPLINE3) {
     mx = static_cast<unsigned*>(workspace(ctx, "sc_chain", size_t(s.nt + 1) * sizeof(unsigned)));
     VB_CUDA(cudaMemsetAsync(mx, 0, size_t(s.nt + 1) * sizeof(unsigned), ctx->stream));
     k_maxabs_bits<<<blocks_for(N, 256), 256, 0, ctx->stream>>>(N, psi + size_t(s.nt) * N,
@@ -1123,15 +1154,22 @@ int sl_characteristics(vreg_ctx ctx, const Slab& s, const float* v3, int degree,
   }
   const bool dist = ctx->nranks > 1;
   const double dt = s.dt();
+  // midpoint samples come from v itself or, for the B-spline, its coefficients
+  const float* vs = v3;
+  if (degree == VREG_INTERP_BSPLINE3) {
+    float* c = static_cast<float*>(workspace(ctx, "bs_v", 3 * N * sizeof(float)));
+    bspline_prefilter(ctx, s, 3, v3, c);
+    vs = c;
+  }
   Ghosts g1, g2, g3;
   if (dist) {
     // ghost width from the midpoint displacement bound dt max|v1| / h1
     const double vmax1 = reduce(ctx, s, 1, v3, v3, true);
-    int G = int(std::floor(dt * vmax1 / s.h(0))) + (degree == 3 ? 3 : 2);
+    int G = int(std::floor(dt * vmax1 / s.h(0))) + (degree != 1 ? 3 : 2);
     require(G <= 2 * s.n1, VREG_ECONFIG, "displacement exceeds twice the domain");
-    g1 = halo_exchange(ctx, s, v3, G, "chars_g1", T_INTERP_COMM, C_GHOST_INTERP);
-    g2 = halo_exchange(ctx, s, v3 + N, G, "chars_g2", T_INTERP_COMM, C_GHOST_INTERP);
-    g3 = halo_exchange(ctx, s, v3 + 2 * N, G, "chars_g3", T_INTERP_COMM, C_GHOST_INTERP);
+    g1 = halo_exchange(ctx, s, vs, G, "chars_g1", T_INTERP_COMM, C_GHOST_INTERP);
+    g2 = halo_exchange(ctx, s, vs + N, G, "chars_g2", T_INTERP_COMM, C_GHOST_INTERP);
+    g3 = halo_exchange(ctx, s, vs + 2 * N, G, "chars_g3", T_INTERP_COMM, C_GHOST_INTERP);
   }
   Timed t(ctx, T_SL, "sl_characteristics");
   const Geo g = geo_of(s);
@@ -1142,15 +1180,15 @@ int sl_characteristics(vreg_ctx ctx, const Slab& s, const float* v3, int degree,
   int ext[3];
   const int T[3] = {TT1, TT2, TT3};
   for (int a = 0; a < 3; ++a)
-    ext[a] = T[a] + (degree == 3 ? 3 : 1) + 2 * int(std::floor(dt * vmax / s.h(a))) + 2;
+    ext[a] = T[a] + (degree != 1 ? 3 : 1) + 2 * int(std::floor(dt * vmax / s.h(a))) + 2;
   ext[2] = ((ext[2] + 3 + 3) / 4) * 4;
   const int words = std::min(BOX_CAP, ext[0] * ext[1] * BOX_PITCH);
   const size_t smem = size_t(words) * sizeof(float);
   SL_DISPATCH(degree, dist,
               (tile_kernel(k_chars_tile<DEG, DIST>)<<<tile_grid(s), TILE_THREADS, smem,
                                                       ctx->stream>>>(
-                  g, src_of<DIST>(v3, g1), src_of<DIST>(v3 + N, g2),
-                  src_of<DIST>(v3 + 2 * N, g3), v3, m1, m2, m3, c1, c2, c3, words, disp3)));
+                  g, src_of<DIST>(vs, g1), src_of<DIST>(vs + N, g2),
+                  src_of<DIST>(vs + 2 * N, g3), v3, m1, m2, m3, c1, c2, c3, words, disp3)));
   return 0;
 }
 
@@ -1159,24 +1197,26 @@ void sl_source_factor(vreg_ctx ctx, const Slab& s, const float* d, const float* 
   check_degree(degree);
   const CharsInfo ci = chars_info(ctx, s, disp_bwd3, flags, degree);
   const bool dist = ctx->nranks > 1 && !ci.identity;
+  // gathered field: d, or its B-spline coefficients; the own term uses d
+  const float* dsrc = ci.identity ? d : gather_source(ctx, s, degree, d, "bs_coef");
   Ghosts gh;
-  if (dist) gh = halo_exchange(ctx, s, d, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
+  if (dist) gh = halo_exchange(ctx, s, dsrc, ci.G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
   Timed t(ctx, T_SL);
   const Geo g = geo_of(s);
   const dim3 grid = sl_grid(s), block(BX, BY);
   const float half = float(0.5 * s.dt());
   if (!ci.identity) {
     const TileLaunch tl = tile_table(ctx, s, disp_bwd3, degree, false);
-    if (use_pipe(s, {d, disp_bwd3, q})) {
-      gather_pipe<3>(ctx, s, degree, dist, d, gh, tl.boxes, disp_bwd3, d, q, half, 0, nullptr,
-                     kAllLayers, (s.n1l + TT1 - 1) / TT1);
+    if (use_pipe(s, {dsrc, d, disp_bwd3, q})) {
+      gather_pipe<3>(ctx, s, degree, dist, dsrc, gh, tl.boxes, disp_bwd3, d, q, half, 0,
+                     nullptr, kAllLayers, (s.n1l + TT1 - 1) / TT1);
       return;
     }
     SL_DISPATCH(degree, dist,
                 (tile_kernel(k_gather_tile<DEG, DIST, 3>)<<<tile_grid(s), TILE_THREADS, tl.smem,
                                                              ctx->stream>>>(
-                    g, src_of<DIST>(d, gh), tl.boxes, disp_bwd3, d, q, nullptr, nullptr, half, 0,
-                    nullptr, kAllLayers)));
+                    g, src_of<DIST>(dsrc, gh), tl.boxes, disp_bwd3, d, q, nullptr, nullptr, half,
+                    0, nullptr, kAllLayers)));
     return;
   }
   SL_DISPATCH(degree, dist,

@@ -59,10 +59,26 @@ __device__ __forceinline__ int wrap1(int b, int n) {
   return b < 0 ? b + n : (b >= n ? b - n : b);
 }
 
-// Lagrange basis on offsets {-1,0,1,2} (interp.cpp:26-35) / linear.
+// Interpolation bases, by template DEG: 1 linear, 3 cubic Lagrange (the
+// reference's two, interp.cpp:26-35), 4 cubic B-spline (B200 extension named
+// by the north star; evaluated on prefiltered coefficients, spline.cu).
+// Both cubic bases use the 4 nodes {-1, 0, 1, 2} around floor(x).
+template <int DEG>
+struct Basis {
+  static constexpr int NN = DEG == 1 ? 2 : 4;    // taps per axis
+  static constexpr int O0 = DEG == 1 ? 0 : -1;   // offset of the first tap
+};
+
 template <int DEG>
 __device__ __forceinline__ void lagrange_weights(float s, float* w) {
-  if constexpr (DEG == 3) {
+  if constexpr (DEG == 4) {
+    // cubic B-spline: ((1-s)^3, 3s^3 - 6s^2 + 4, -3s^3 + 3s^2 + 3s + 1, s^3) / 6
+    const float ms = 1.0f - s, s2 = s * s, s3 = s2 * s;
+    w[0] = ms * ms * ms * (1.0f / 6.0f);
+    w[1] = __fmaf_rn(3.0f, s3, __fmaf_rn(-6.0f, s2, 4.0f)) * (1.0f / 6.0f);
+    w[2] = __fmaf_rn(-3.0f, s3, __fmaf_rn(3.0f, s2, __fmaf_rn(3.0f, s, 1.0f))) * (1.0f / 6.0f);
+    w[3] = s3 * (1.0f / 6.0f);
+  } else if constexpr (DEG == 3) {
     // factored: q = -s (1-s) / 6, r = (s+1)(2-s) / 2; w = (q (2-s), r (1-s), r s, q (s+1))
     const float ms = 1.0f - s, sp = s + 1.0f, ns2 = 2.0f - s;
     const float q = __fmul_rn(__fmul_rn(s, ms), -1.0f / 6.0f);
@@ -117,8 +133,8 @@ struct DstField {
 // DIST, wrapped otherwise), row offsets along x2, columns along x3.
 template <int DEG>
 struct Stencil {
-  static constexpr int NN = DEG + 1;
-  static constexpr int O0 = DEG == 3 ? -1 : 0;
+  static constexpr int NN = Basis<DEG>::NN;
+  static constexpr int O0 = Basis<DEG>::O0;
   int p1[NN];
   int r2[NN];
   int c3[NN];

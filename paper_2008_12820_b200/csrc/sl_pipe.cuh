@@ -178,7 +178,7 @@ __device__ __forceinline__ void pipe_produce(const Geo& g, const Field& src, con
 
 template <int DEG>
 struct PipeStencil {
-  static constexpr int NN = DEG + 1, O0 = DEG == 3 ? -1 : 0;
+  static constexpr int NN = Basis<DEG>::NN, O0 = Basis<DEG>::O0;
   int base;
   float w1[NN], w2[NN], w3[NN];
 
@@ -203,7 +203,7 @@ struct PipeStencil {
 
   __device__ __forceinline__ float gather(int e2, const float* sbox) const {
     const int e23 = e2 * PIPE_P3;
-    if constexpr (DEG == 3) {
+    if constexpr (NN == 4) {
       const float2 w3a = make_float2(w3[0], w3[1]), w3b = make_float2(w3[2], w3[3]);
       float2 w23[NN][2];
 #pragma unroll

@@ -102,7 +102,7 @@ template <int DEG>
 __global__ void __launch_bounds__(TILE_THREADS) k_tile_boxes(Geo g, const float* __restrict__ D,
                                                              int* __restrict__ table,
                                                              int* __restrict__ max_words) {
-  constexpr int NN = DEG + 1, O0 = DEG == 3 ? -1 : 0;
+  constexpr int NN = Basis<DEG>::NN, O0 = Basis<DEG>::O0;
   __shared__ int smn[3], smx[3];
   if (threadIdx.x < 3) {
     smn[threadIdx.x] = 1 << 30;
@@ -322,7 +322,7 @@ __device__ __forceinline__ void flush_box_fixed(const Geo& g, const DstField<DIS
 
 template <int DEG>
 struct BoxStencil {
-  static constexpr int NN = DEG + 1, O0 = DEG == 3 ? -1 : 0;
+  static constexpr int NN = Basis<DEG>::NN, O0 = Basis<DEG>::O0;
   int base;  // smem word index of tap (0,0,0)
   float w1[NN], w2[NN], w3[NN];
 
@@ -347,7 +347,7 @@ struct BoxStencil {
 
   __device__ __forceinline__ float gather(const TileBox& b, const float* sbox) const {
     const int e23 = b.ext[1] * BOX_PITCH;
-    if constexpr (DEG == 3) {
+    if constexpr (NN == 4) {
       // packed fp32x2 (FFMA2): tap pairs (c0,c1), (c2,c3) of each row with
       // the outer-product weights w2[bb] w3[c]; planes folded with w1.
       const float2 w3a = make_float2(w3[0], w3[1]), w3b = make_float2(w3[2], w3[3]);

@@ -46,9 +46,10 @@ namespace {
 constexpr unsigned kT = 256;
 
 // F *= scale * sym(k), sym = beta |k|^2 (zero mode: unit or 0) [regop] or
-// 1 / (beta |k|^2) (zero mode 1/beta) [inv_regop] (spectral.cpp:48-93).
+// 1 / (beta |k|^2) (zero mode 1/beta) [inv_regop] (spectral.cpp:48-93);
+// order 2: |k|^4 (H2).
 __global__ void k_symbol(SpecDesc d, int ncomp, float2* __restrict__ F, float beta, int inverse,
-                         int unit_zero, float scale) {
+                         int unit_zero, float scale, int order) {
   // one CTA per (component, k1, local k2) row, threads along k3
   const int k2l = blockIdx.x, c = blockIdx.y / d.n1, k1 = blockIdx.y - c * d.n1;
   const float f1 = sfreq(k1, d.n1), f2 = sfreq(k2l + d.k2off, d.n2);
@@ -57,6 +58,7 @@ __global__ void k_symbol(SpecDesc d, int ncomp, float2* __restrict__ F, float be
   for (int k3 = threadIdx.x; k3 < d.h; k3 += blockDim.x) {
     const float f3 = float(k3);
     float sym = f12 + f3 * f3;
+    if (order == 2) sym *= sym;  // H2: |k|^4
     float m;
     if (inverse) {
       if (sym == 0.0f) sym = 1.0f;
@@ -65,6 +67,25 @@ __global__ void k_symbol(SpecDesc d, int ncomp, float2* __restrict__ F, float be
       if (sym == 0.0f) sym = unit_zero ? 1.0f : 0.0f;
       m = scale * (beta * sym);
     }
+    float2 v = R[k3];
+    v.x *= m;
+    v.y *= m;
+    R[k3] = v;
+  }
+}
+
+// Cubic B-spline prefilter: F *= scale / (b(k1) b(k2) b(k3)), b(k) =
+// (2 + cos(2 pi k / n)) / 3 -- the spectrum of the periodic B-spline
+// coefficients that interpolate the field at the nodes (b is the symbol of
+// the node samples 1/6, 2/3, 1/6 of the cubic B-spline).
+__global__ void k_bspline_prefilter(SpecDesc d, int ncomp, float2* __restrict__ F, float scale) {
+  const int k2l = blockIdx.x, c = blockIdx.y / d.n1, k1 = blockIdx.y - c * d.n1;
+  const float b12 = ((2.0f + cospif(2.0f * float(k1) / float(d.n1))) / 3.0f) *
+                    ((2.0f + cospif(2.0f * float(k2l + d.k2off) / float(d.n2))) / 3.0f);
+  float2* R = F + size_t(c) * d.nc + (size_t(k1) * d.n2l + k2l) * d.h;
+  for (int k3 = threadIdx.x; k3 < d.h; k3 += blockDim.x) {
+    const float b = b12 * ((2.0f + cospif(2.0f * float(k3) / float(d.n3))) / 3.0f);
+    const float m = scale / b;
     float2 v = R[k3];
     v.x *= m;
     v.y *= m;
@@ -97,7 +118,8 @@ __global__ void k_leray(SpecDesc d, float2* __restrict__ F, float scale) {
 
 // Per-(component, k2-row) fp64 partial of sum w3 |k|^2 |F|^2 over k3, k1
 // (spectral.cpp:95-118: k2-major fold).
-__global__ void k_seminorm_rows(SpecDesc d, const float2* __restrict__ F, double* __restrict__ rows) {
+__global__ void k_seminorm_rows(SpecDesc d, const float2* __restrict__ F, double* __restrict__ rows,
+                                int order) {
   const int c = blockIdx.y;
   const int k2l = blockIdx.x;
   const int k2 = k2l + d.k2off;
@@ -109,7 +131,8 @@ __global__ void k_seminorm_rows(SpecDesc d, const float2* __restrict__ F, double
     const int k1 = t / d.h, k3 = t % d.h;
     const float f1 = sfreq(k1, d.n1);
     const double w3 = (k3 == 0 || 2 * k3 == d.n3) ? 1.0 : 2.0;
-    const double sym = double(f1) * f1 + double(f2) * f2 + double(k3) * k3;
+    double sym = double(f1) * f1 + double(f2) * f2 + double(k3) * k3;
+    if (order == 2) sym *= sym;
     const float2 v = Fc[(size_t(k1) * d.n2l + k2l) * d.h + k3];
     acc += w3 * sym * (double(v.x) * v.x + double(v.y) * v.y);
   }
@@ -339,7 +362,7 @@ void apply_symbol(vreg_ctx ctx, const SpecDesc& d, int ncomp, float2* F, double 
                   bool unit_zero, double scale) {
   Timed t(ctx, T_FFT, "spec_symbol");
   k_symbol<<<dim3(unsigned(d.n2l), unsigned(ncomp * d.n1)), 128, 0, ctx->stream>>>(
-      d, ncomp, F, float(beta), inverse ? 1 : 0, unit_zero ? 1 : 0, float(scale));
+      d, ncomp, F, float(beta), inverse ? 1 : 0, unit_zero ? 1 : 0, float(scale), ctx->reg_order);
   count_launch(ctx);
   check_launch();
 }
@@ -354,12 +377,41 @@ bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, 
 void spectral_regop(vreg_ctx ctx, const Slab& s, const float* v3, double beta, bool unit_zero,
                     bool inverse, float* out3) {
   require(beta > 0.0, VREG_EPARAM, "regularization beta must be > 0");
+  if (!inverse && ctx->reg_order == 2) {
+    // H2 = beta A(A v) with the unit-weight H1 operator: symbol (|k|^2)^2,
+    // the null mode unit * unit or 0 * 0 -- two separable sweeps where the
+    // grid allows
+    float* tmp = static_cast<float*>(workspace(ctx, "h2_tmp", 3 * s.local() * sizeof(float)));
+    ctx->reg_order = 1;
+    try {
+      spectral_regop(ctx, s, v3, 1.0, unit_zero, false, tmp);
+      spectral_regop(ctx, s, tmp, beta, unit_zero, false, out3);
+    } catch (...) {
+      ctx->reg_order = 2;
+      throw;
+    }
+    ctx->reg_order = 2;
+    return;
+  }
   if (!inverse && regop_separable(ctx, s, v3, beta, out3, unit_zero)) return;
   const SpecDesc d = spec_desc(ctx, s);
   float2* F = spec_buffer(ctx, d, 3, "spec3");
   fft_forward(ctx, s, 3, v3, F);
   apply_symbol(ctx, d, 3, F, beta, inverse, unit_zero, 1.0 / double(s.global()));
   fft_inverse(ctx, s, 3, F, out3);
+}
+
+// Cubic B-spline coefficients of ncomp fields (in == out allowed).
+void bspline_prefilter(vreg_ctx ctx, const Slab& s, int ncomp, const float* in, float* out) {
+  const SpecDesc d = spec_desc(ctx, s);
+  float2* F = spec_buffer(ctx, d, ncomp, ncomp == 3 ? "spec3" : "spec1");
+  fft_forward(ctx, s, ncomp, in, F);
+  Timed t(ctx, T_FFT, "spec_bspline");
+  k_bspline_prefilter<<<dim3(unsigned(d.n2l), unsigned(ncomp * d.n1)), 128, 0, ctx->stream>>>(
+      d, ncomp, F, float(1.0 / double(s.global())));
+  count_launch(ctx);
+  check_launch();
+  fft_inverse(ctx, s, ncomp, F, out);
 }
 
 void h0_pointwise(vreg_ctx ctx, const Slab& s, const float* s3, const float* g3, float* out3) {
@@ -390,7 +442,7 @@ int vreg_seminorm(vreg_ctx ctx, const vreg_grid* g, const float* v3, double* out
     float2* F = spec_buffer(ctx, d, 3, "spec3");
     fft_forward(ctx, s, 3, v3, F);
     double* rows = static_cast<double*>(workspace(ctx, "semi_rows", sizeof(double) * 3 * s.n2));
-    k_seminorm_rows<<<dim3(d.n2l, 3), kT, 0, ctx->stream>>>(d, F, rows);
+    k_seminorm_rows<<<dim3(d.n2l, 3), kT, 0, ctx->stream>>>(d, F, rows, ctx->reg_order);
     count_launch(ctx);
     check_launch();
     const double* src = rows;

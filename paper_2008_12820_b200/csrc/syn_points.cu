@@ -10,6 +10,8 @@
 
 namespace vb {
 
+void bspline_prefilter(vreg_ctx ctx, const Slab& s, int ncomp, const float* in, float* out);
+
 namespace {
 
 __global__ void k_syn_template(int n1l, int off, int n2, int n3, double h1, double h2, double h3,
@@ -66,9 +68,9 @@ __device__ __forceinline__ void point_stencil(const Geo& g, const double* xyz, d
   lagrange_weights<DEG>(s1, st.w1);
   lagrange_weights<DEG>(s2, st.w2);
   lagrange_weights<DEG>(s3, st.w3);
-  constexpr int O0 = DEG == 3 ? -1 : 0;
+  constexpr int O0 = Basis<DEG>::O0;
 #pragma unroll
-  for (int o = 0; o < DEG + 1; ++o) {
+  for (int o = 0; o < Basis<DEG>::NN; ++o) {
     st.p1[o] = wrap1(b1 + O0 + o, g.n1);
     st.r2[o] = wrap1(b2 + O0 + o, g.n2) * g.n3;
     st.c3[o] = wrap1(b3 + O0 + o, g.n3);
@@ -119,7 +121,8 @@ Geo point_geo(const Slab& s) {
 }
 
 void check_points(vreg_ctx ctx, const double* xyz, int64_t m, int degree) {
-  require(degree == 1 || degree == 3, VREG_EPARAM, "interpolation degree must be 1 or 3");
+  require(degree == 1 || degree == 3 || degree == VREG_INTERP_BSPLINE3, VREG_EPARAM,
+          "interpolation degree must be 1, 3 or 4 (cubic B-spline)");
   require(ctx->nranks == 1, VREG_ECONFIG, "point queries are single-rank");
   int* flag = static_cast<int*>(workspace(ctx, "nan_flag", sizeof(int)));
   VB_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
@@ -169,7 +172,12 @@ int vreg_interp_points(vreg_ctx ctx, const vreg_grid* gr, const float* f, const 
     check_points(ctx, xyz, m, degree);
     if (m == 0) return;
     const Geo g = point_geo(s);
-    if (degree == 3)
+    if (degree == VREG_INTERP_BSPLINE3) {  // evaluate the B-spline coefficients
+      float* c = static_cast<float*>(workspace(ctx, "bs_points", s.local() * sizeof(float)));
+      bspline_prefilter(ctx, s, 1, f, c);
+      k_interp_points<4><<<blocks_for(size_t(m), 256), 256, 0, ctx->stream>>>(
+          g, c, xyz, m, s.h(0), s.h(1), s.h(2), out);
+    } else if (degree == 3)
       k_interp_points<3><<<blocks_for(size_t(m), 256), 256, 0, ctx->stream>>>(
           g, f, xyz, m, s.h(0), s.h(1), s.h(2), out);
     else
@@ -187,6 +195,19 @@ int vreg_scatter_points(vreg_ctx ctx, const vreg_grid* gr, const double* xyz, co
     check_points(ctx, xyz, m, degree);
     if (m == 0) return;
     const Geo g = point_geo(s);
+    if (degree == VREG_INTERP_BSPLINE3) {  // acc += P B^T z (P the symmetric prefilter)
+      float* t = static_cast<float*>(workspace(ctx, "bs_points", s.local() * sizeof(float)));
+      VB_CUDA(cudaMemsetAsync(t, 0, s.local() * sizeof(float), ctx->stream));
+      k_scatter_points<4><<<blocks_for(size_t(m), 256), 256, 0, ctx->stream>>>(
+          g, t, xyz, z, m, s.h(0), s.h(1), s.h(2));
+      count_launch(ctx);
+      check_launch();
+      bspline_prefilter(ctx, s, 1, t, t);
+      vreg_grid gg{s.n1, s.n2, s.n3, s.nt};
+      const int st = vreg_axpy(ctx, &gg, 1, 1.0, t, acc);
+      require(st == VREG_OK, st, "axpy failed");
+      return;
+    }
     if (degree == 3)
       k_scatter_points<3><<<blocks_for(size_t(m), 256), 256, 0, ctx->stream>>>(
           g, acc, xyz, z, m, s.h(0), s.h(1), s.h(2));

@@ -113,6 +113,11 @@ class Context:
         independent of the GPU count); default fp32 L2 reductions."""
         check(lib().vreg_ctx_set_deterministic(self.h, int(on)))
 
+    def set_reg_order(self, order=1):
+        """Regularisation order of regop / inv_regop / seminorm / h0 / the GN
+        matvec: 1 = H1 (|k|^2, the reference), 2 = H2 (|k|^4)."""
+        check(lib().vreg_ctx_set_reg_order(self.h, int(order)))
+
     def enable_timers(self, on=True):
         check(lib().vreg_ctx_enable_timers(self.h, int(on)))
 

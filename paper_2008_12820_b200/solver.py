@@ -40,7 +40,7 @@ class VregConfig(C.Structure):
         ("interp_degree", C.c_int), ("cache_state_gradient", C.c_int), ("fixed_gn", C.c_int),
         ("fixed_pcg", C.c_int), ("hessian_adjoint", C.c_int), ("nt", C.c_int),
         ("armijo_c", C.c_double), ("armijo_shrink", C.c_double), ("armijo_max_trials", C.c_int),
-        ("h0_inner_cap", C.c_int), ("pcg_fp64", C.c_int),
+        ("h0_inner_cap", C.c_int), ("pcg_fp64", C.c_int), ("reg_order", C.c_int),
     ]
 
 
@@ -68,6 +68,7 @@ class Config:
     armijo_max_trials: int = 10
     h0_inner_cap: int = 100
     pcg_fp64: bool = True
+    reg_order: int = 1  # 1 = H1 (reference), 2 = H2 (B200 extension)
 
     def to_c(self) -> VregConfig:
         c = VregConfig()

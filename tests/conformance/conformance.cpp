@@ -35,6 +35,7 @@ static std::vector<double> flat(const VectorField& v) {
   for (int c = 0; c < 3; ++c) o.insert(o.end(), v.comp(c).v.begin(), v.comp(c).v.end());
   return o;
 }
+static std::vector<double> flat(const ScalarField& f) { return f.v; }
 
 int main() {
   const int n = 32, nt = 4;
@@ -75,6 +76,9 @@ int main() {
   report("objective", std::abs(Jc.total / Js.total - 1));
   report("mismatch", std::abs(Jc.mismatch / Js.mismatch - 1));
   report("hessian_matvec", rel(Hc.to_host(), flat(Hs)));
+  // engine.hpp:63-66 round trip: from_global / to_global(_v)
+  report("to_global", rel(flat(ce.to_global(ce.from_global(m0))), flat(m0)));
+  report("to_global_v", rel(flat(ce.to_global_v(Hc)), Hc.to_host()));
 
   // pcg on the GN Hessian with the InvA preconditioner, 5 iterations
   PcgOptions opt;

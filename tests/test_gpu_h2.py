@@ -1,0 +1,122 @@
+"""H2 regularisation (B200 extension named by the north star; the reference
+implements H1 only, spectral.cpp:61-63, so there is no oracle run).
+
+Pinned by analytic known-answer tests instead:
+  * single Fourier modes are eigenfunctions: regop v = beta |k|^4 v,
+    inv_regop v = v / (beta |k|^4), |v|^2_H2 = |k|^4 ||v||^2, on the
+    separable-pass grid (32^3) and the cuFFT grid (24 x 20 x 28);
+  * null mode: unit (1 / beta for the inverse) as for H1;
+  * H2 = (H1 with beta = 1) applied twice, on random fields;
+  * the reduced gradient of the H2 objective is its derivative: a central
+    difference of J along a direction matches <g, d> to 1e-3;
+  * an H2 registration decreases the mismatch.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2008_12820_b200 import VregGrid
+from paper_2008_12820_b200.solver import Config, Solver
+
+pytestmark = pytest.mark.gpu
+
+
+def mode_field(shape, k, comp):
+    n1, n2, n3 = shape
+    x = [np.arange(n) * 2 * math.pi / n for n in shape]
+    X1, X2, X3 = np.meshgrid(*x, indexing="ij")
+    f = np.zeros((3,) + tuple(shape))
+    f[comp] = np.cos(k[0] * X1 + k[1] * X2 + k[2] * X3)
+    return f
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float32, device="cuda")
+
+
+def host(t):
+    return t.detach().double().cpu().numpy()
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture
+def h2(ctx):
+    ctx.set_reg_order(2)
+    yield ctx
+    ctx.set_reg_order(1)
+
+
+@pytest.mark.parametrize("shape", [(32, 32, 32), (24, 20, 28)])
+@pytest.mark.parametrize("k,comp", [((2, 1, 3), 0), ((0, 4, 1), 2), ((5, 0, 0), 1)])
+def test_h2_single_modes(h2, shape, k, comp):
+    ctx = h2
+    g = VregGrid(*shape, 4)
+    beta = 3e-3
+    v = mode_field(shape, k, comp)
+    k4 = float(sum(a * a for a in k)) ** 2
+    out = host(ctx.regop(g, dev(v), beta, False))
+    assert rel(out, beta * k4 * v) < 2e-6
+    inv = host(ctx.inv_regop(g, dev(v), beta))
+    assert rel(inv, v / (beta * k4)) < 2e-6
+    sn = ctx.seminorm(g, dev(v))
+    norm2 = (v ** 2).sum() * (2 * math.pi) ** 3 / np.prod(shape)
+    assert abs(sn / (k4 * norm2) - 1) < 2e-6
+
+
+@pytest.mark.parametrize("shape", [(32, 32, 32), (24, 20, 28)])
+def test_h2_null_mode_and_composition(ctx, shape):
+    g = VregGrid(*shape, 4)
+    rng = np.random.default_rng(7)
+    v = rng.standard_normal((3,) + shape)
+    beta = 2e-2
+    ctx.set_reg_order(1)
+    a1 = ctx.regop(g, dev(v), 1.0, True)
+    twice = host(ctx.regop(g, a1, beta, True))
+    ctx.set_reg_order(2)
+    try:
+        h2 = host(ctx.regop(g, dev(v), beta, True))
+        assert rel(h2, twice) < 1e-5
+        c = np.ones((3,) + shape)
+        assert rel(host(ctx.regop(g, dev(c), beta, True)), beta * c) < 1e-6   # unit null mode
+        assert rel(host(ctx.inv_regop(g, dev(c), beta)), c / beta) < 1e-6     # 1/beta
+        assert np.abs(host(ctx.regop(g, dev(c), beta, False))).max() < 1e-6  # zero null mode
+    finally:
+        ctx.set_reg_order(1)
+
+
+def test_h2_gradient_is_the_derivative(ctx):
+    """<g, d> against (J(v + e d) - J(v - e d)) / 2e for the H2 objective."""
+    n, beta = 32, 1e-2
+    cfg = Config(continuation=False, beta_target=beta, reg_order=2)
+    s = Solver(ctx, n, cfg)
+    s.syn_images()
+    v = (0.5 * ctx.syn_velocity(s.grid)).contiguous()
+    s.linearize(v, beta)
+    g = s.gradient().double()
+    d = torch.sin(torch.arange(v.numel(), device="cuda", dtype=torch.float64) * 1e-3).reshape(v.shape)
+    h3 = (2 * math.pi / n) ** 3
+    gd = float((g * d).sum() * h3)
+    eps = 1e-2
+    Js = []
+    for sgn in (1, -1):
+        s.linearize((v.double() + sgn * eps * d).float().contiguous(), beta)
+        Js.append(s.objective()["total"])
+    fd = (Js[0] - Js[1]) / (2 * eps)
+    assert abs(fd / gd - 1) < 1e-3, (fd, gd)
+    s.close()
+
+
+def test_h2_registration_reduces_mismatch(ctx):
+    n = 32
+    s = Solver(ctx, n, Config(continuation=False, beta_target=1e-3, reg_order=2, fixed_gn=2,
+                              fixed_pcg=5, precond="2linvh0"))
+    s.syn_images()
+    v, rep, _ = s.register()
+    assert rep["final_mismatch"] < 0.2 * rep["initial_mismatch"]
+    assert torch.isfinite(v).all()
+    s.close()

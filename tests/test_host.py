@@ -52,9 +52,10 @@ def test_config_layout_matches_reference_config():
     from paper_2008_12820_b200 import _lib
     from paper_2008_12820_b200.solver import Config, VregConfig
     # the reference's RegistrationConfig fields in order (optim.hpp:16-37),
-    # then the B200 extension pcg_fp64 (fp64 PCG iterates)
+    # then the B200 extensions (fp64 PCG iterates, H2 regularisation)
     names = [f[0] for f in VregConfig._fields_]
-    assert names[:-1] == [f[0] for f in ref.VrefConfig._fields_] and names[-1] == "pcg_fp64"
+    assert names[:-2] == [f[0] for f in ref.VrefConfig._fields_]
+    assert names[-2:] == ["pcg_fp64", "reg_order"]
     assert VregConfig.pcg_fp64.offset >= C.sizeof(ref.VrefConfig) - 4
     c = VregConfig()
     _lib.lib().vreg_config_default(C.byref(c))

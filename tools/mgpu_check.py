@@ -25,6 +25,7 @@ from paper_2008_12820_b200.solver import Config, Solver  # noqa: E402
 
 
 def run(ctx, dims, beta):
+    big = dims[0] * dims[1] * dims[2] > 128 ** 3  # 512^3: kernels and operators only
     cfg = Config(continuation=False, beta_target=beta, precond="inva")
     s = Solver(ctx, dims, cfg)
     s.syn_images()
@@ -39,18 +40,21 @@ def run(ctx, dims, beta):
     Hd = s.matvec(vt)
     ctx.set_deterministic(False)
     P, _ = s.precond("inva", vt, 0.5)
+    P2, _ = s.precond("2linvh0", vt, 0.5)
     m0, m1 = s.images()
+    out = {"J": J, "grad": ctx.to_global(g, grad), "H": ctx.to_global(g, H),
+           "Hdet": ctx.to_global(g, Hd), "P": ctx.to_global(g, P), "P2": ctx.to_global(g, P2),
+           "m1": ctx.to_global(g, m1)}
+    s.close()
+    if big:
+        return out
     # optimize-then-discretize (SL incremental adjoint) Hessian, optim.hpp:125-128
     s_sl = Solver(ctx, dims, Config(continuation=False, beta_target=beta, precond="inva",
                                     hessian_adjoint=1))
     s_sl.syn_images()
     s_sl.linearize(v, beta)
-    H_sl = ctx.to_global(g, s_sl.matvec(vt))
+    out["H_sl"] = ctx.to_global(g, s_sl.matvec(vt))
     s_sl.close()
-    out = {"J": J, "grad": ctx.to_global(g, grad), "H": ctx.to_global(g, H),
-           "Hdet": ctx.to_global(g, Hd),
-           "P": ctx.to_global(g, P), "m1": ctx.to_global(g, m1), "H_sl": H_sl}
-    s.close()
     cfg2 = Config(continuation=False, beta_target=beta, precond="inva", fixed_gn=2, fixed_pcg=3)
     s2 = Solver(ctx, dims, cfg2)
     s2.syn_images()
@@ -68,9 +72,6 @@ def run(ctx, dims, beta):
     cfg3 = Config(continuation=False, beta_target=beta, precond="2linvh0", fixed_gn=2, fixed_pcg=3)
     s3 = Solver(ctx, dims, cfg3)
     s3.syn_images()
-    s3.linearize(v, beta)
-    P2, st = s3.precond("2linvh0", vt, 0.5)
-    out["P2"] = ctx.to_global(g, P2)
     vv3, rep3, _ = s3.register()
     out["solve2l"] = rep3
     out["v2l"] = ctx.to_global(g, vv3)
@@ -157,17 +158,20 @@ def main():
         res["mismatch_rel"] = abs(dist_out["J"]["mismatch"] / ref["J"]["mismatch"] - 1)
         for k in ("m1", "grad", "H", "Hdet", "H_sl", "P", "v", "regop", "restrict", "high_pass",
                   "P2", "v2l"):
-            res[f"{k}_rel"] = rel(dist_out[k], ref[k].astype(np.float64))
-        res["solve_mismatch_rel"] = abs(dist_out["solve"]["final_mismatch"] /
-                                        ref["solve"]["final_mismatch"] - 1)
-        res["solve2l_mismatch_rel"] = abs(dist_out["solve2l"]["final_mismatch"] /
-                                          ref["solve2l"]["final_mismatch"] - 1)
+            if k in dist_out:
+                res[f"{k}_rel"] = rel(dist_out[k], ref[k].astype(np.float64))
         ok = (res["m1_rel"] < 1e-6 and res["J_rel"] < 1e-6 and res["grad_rel"] < 1e-5 and
-              res["H_rel"] < 1e-5 and res["H_sl_rel"] < 1e-5 and res["P_rel"] < 1e-5 and res["v_rel"] < 1e-4 and
-              res["solve_mismatch_rel"] < 1e-4 and res["restrict_rel"] < 1e-5 and
-              res["high_pass_rel"] < 1e-5 and res["P2_rel"] < 1e-4 and res["v2l_rel"] < 1e-4 and
-              res["solve2l_mismatch_rel"] < 1e-4 and res["regop_rel"] == 0.0 and
+              res["H_rel"] < 1e-5 and res["P_rel"] < 1e-5 and res["P2_rel"] < 1e-4 and
               res["Hdet_rel"] == 0.0)
+        if "solve" in dist_out:
+            res["solve_mismatch_rel"] = abs(dist_out["solve"]["final_mismatch"] /
+                                            ref["solve"]["final_mismatch"] - 1)
+            res["solve2l_mismatch_rel"] = abs(dist_out["solve2l"]["final_mismatch"] /
+                                              ref["solve2l"]["final_mismatch"] - 1)
+            ok = ok and (res["H_sl_rel"] < 1e-5 and res["v_rel"] < 1e-4 and
+                         res["solve_mismatch_rel"] < 1e-4 and res["restrict_rel"] < 1e-5 and
+                         res["high_pass_rel"] < 1e-5 and res["v2l_rel"] < 1e-4 and
+                         res["solve2l_mismatch_rel"] < 1e-4 and res["regop_rel"] == 0.0)
         res["ok"] = ok
         print(json.dumps(res), flush=True)
         single.close()
