@@ -129,6 +129,7 @@ struct vreg_ctx_s {
   // regularisation order of the spectral operators: 1 = H1 (symbol |k|^2,
   // the reference's spectral.cpp:61-63), 2 = H2 (|k|^4, B200 extension)
   int reg_order = 1;
+  double tl_beta = 0;  // beta_pc of the last two-level begin (read by its end)
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;
   // regulariser x2-slab transposes by copy engine into the peers' buffers

@@ -123,10 +123,10 @@ __global__ void k_to_f32(size_t n, const T* __restrict__ x, float* __restrict__ 
 
 enum FoldMode { F_R0 = 0, F_RZ, F_PQ, F_RR };
 
-// Fold the partials [rank][comp][plane][chunk] in the reference association
-// (per component: planes in global order, chunks in order; components summed
-// after scaling by h^3, field.hpp:150-175) and apply the CG recurrence of
-// `mode`. Single CTA; ends by setting the loop condition (cond != 0).
+// Fold the partials [rank][comp][plane][chunk] (per component over the
+// global planes, field.hpp:150-175 up to association; components summed
+// after scaling by h^3) and apply the CG recurrence of `mode`. Single CTA;
+// ends by setting the loop condition (cond != 0).
 __global__ void __launch_bounds__(KT) k_fold(int mode, int nranks, int n1l, int chunks,
                                              double h3, const double* __restrict__ part,
                                              KrylovState* __restrict__ st,
@@ -142,13 +142,23 @@ __global__ void __launch_bounds__(KT) k_fold(int mode, int nranks, int n1l, int 
     plsum[e] = s;
   }
   __syncthreads();
+  // per component: lane l folds the global planes [l B, (l + 1) B) in order,
+  // then a fixed shuffle tree -- an association independent of the rank
+  // count (planes are in global order), so p GPUs give bitwise the same sums
+  __shared__ double comp[3];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (w < 3) {
+    const int B = (n1 + 31) / 32;
+    double a = 0.0;
+    for (int i = l * B; i < min(n1, (l + 1) * B); ++i) a += plsum[w * n1 + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+    if (l == 0) comp[w] = a;
+  }
+  __syncthreads();
   if (threadIdx.x != 0) return;
   double total = 0.0;
-  for (int c = 0; c < 3; ++c) {
-    double comp = 0.0;
-    for (int i = 0; i < n1; ++i) comp += plsum[c * n1 + i];
-    total += comp * h3;
-  }
+  for (int c = 0; c < 3; ++c) total += comp[c] * h3;
   KrylovState& S = *st;
   // a body entered after the solve stopped (the WHILE condition is checked
   // before each body) leaves the state alone: pad marks such a pass

@@ -50,14 +50,16 @@ constexpr unsigned kT = 256;
 // order 2: |k|^4 (H2).
 __global__ void k_symbol(SpecDesc d, int ncomp, float2* __restrict__ F, float beta, int inverse,
                          int unit_zero, float scale, int order) {
-  // one CTA per (component, k1, local k2) row, threads along k3
-  const int k2l = blockIdx.x, c = blockIdx.y / d.n1, k1 = blockIdx.y - c * d.n1;
-  const float f1 = sfreq(k1, d.n1), f2 = sfreq(k2l + d.k2off, d.n2);
-  const float f12 = f1 * f1 + f2 * f2;
-  float2* R = F + size_t(c) * d.nc + (size_t(k1) * d.n2l + k2l) * d.h;
-  for (int k3 = threadIdx.x; k3 < d.h; k3 += blockDim.x) {
-    const float f3 = float(k3);
-    float sym = f12 + f3 * f3;
+  // flat over every (component, k1, local k2, k3) element: one row of
+  // n3/2 + 1 per CTA left most threads idle on the odd tail element
+  const unsigned total = unsigned(ncomp) * unsigned(d.n1) * unsigned(d.n2l) * unsigned(d.h);
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const unsigned k3 = e % unsigned(d.h), row = e / unsigned(d.h);
+    const unsigned k2l = row % unsigned(d.n2l), k1 = (row / unsigned(d.n2l)) % unsigned(d.n1);
+    const float f1 = sfreq(int(k1), d.n1), f2 = sfreq(int(k2l) + d.k2off, d.n2),
+                f3 = float(k3);
+    float sym = f1 * f1 + f2 * f2 + f3 * f3;
     if (order == 2) sym *= sym;  // H2: |k|^4
     float m;
     if (inverse) {
@@ -67,10 +69,10 @@ __global__ void k_symbol(SpecDesc d, int ncomp, float2* __restrict__ F, float be
       if (sym == 0.0f) sym = unit_zero ? 1.0f : 0.0f;
       m = scale * (beta * sym);
     }
-    float2 v = R[k3];
+    float2 v = F[e];
     v.x *= m;
     v.y *= m;
-    R[k3] = v;
+    F[e] = v;
   }
 }
 
@@ -197,6 +199,55 @@ __global__ void k_restrict(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3,
   }
 }
 
+// Inverse regularisation symbol 1 / (beta |k|^2) (|k|^4 for H2), zero mode
+// 1 / beta (spectral.cpp:72-93); even in every wavenumber.
+__device__ __forceinline__ float inv_symbol(int nu1, int nu2, int nu3, float beta, int order) {
+  float sym = float(nu1) * nu1 + float(nu2) * nu2 + float(nu3) * nu3;
+  if (order == 2) sym *= sym;
+  if (sym == 0.0f) sym = 1.0f;
+  return 1.0f / (beta * sym);
+}
+
+// Both restrictions of the two-level apply from one pass over the fine
+// spectrum: Fr = restrict(F) and Fs = restrict(InvA F). Restriction only
+// pairs alias partners of equal |k| (the coarse Nyquist lines), so
+// restrict(InvA F) = InvA_c restrict(F) mode by mode.
+__global__ void k_restrict_pair(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3,
+                                const float2* __restrict__ Ff, float2* __restrict__ Fr,
+                                float2* __restrict__ Fs, float scale, float beta, int order) {
+  const int hc = nc3 / 2 + 1, hf = nf3 / 2 + 1;
+  const size_t ncc = size_t(nc1) * nc2 * hc, ncf = size_t(nf1) * nf2 * hf;
+  const unsigned total = 3u * unsigned(ncc);
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int c = int(e / unsigned(ncc));
+    const unsigned r = e - unsigned(c) * unsigned(ncc);
+    int k1, k2, k3;
+    split3(r, unsigned(hc), unsigned(nc2), k1, k2, k3);
+    const int nu1 = k1 <= nc1 / 2 ? k1 : k1 - nc1;
+    const int nu2 = k2 <= nc2 / 2 ? k2 : k2 - nc2;
+    const int nu3 = k3;
+    int p1[2] = {nu1, 0}, p2[2] = {nu2, 0}, p3[2] = {nu3, 0};
+    int c1 = 1, c2 = 1, c3 = 1;
+    if (abs(nu1) == nc1 / 2) { p1[0] = nc1 / 2; p1[1] = -nc1 / 2; c1 = 2; }
+    if (abs(nu2) == nc2 / 2) { p2[0] = nc2 / 2; p2[1] = -nc2 / 2; c2 = 2; }
+    if (abs(nu3) == nc3 / 2) { p3[0] = nc3 / 2; p3[1] = -nc3 / 2; c3 = 2; }
+    const float2* F = Ff + size_t(c) * ncf;
+    float ax = 0.f, ay = 0.f;
+    for (int a = 0; a < c1; ++a)
+      for (int b = 0; b < c2; ++b)
+        for (int q = 0; q < c3; ++q) {
+          const float2 v = full_at(F, nf1, nf2, nf3, pmod(p1[a], nf1), pmod(p2[b], nf2),
+                                   pmod(p3[q], nf3));
+          ax += v.x;
+          ay += v.y;
+        }
+    const float m = inv_symbol(nu1, nu2, nu3, beta, order);
+    Fr[e] = make_float2(ax * scale, ay * scale);
+    Fs[e] = make_float2(ax * scale * m, ay * scale * m);
+  }
+}
+
 // Fine half spectrum from the coarse one: coarse modes split evenly over
 // their fine partners, zero outside the band (spectral.cpp:176-203).
 __device__ __forceinline__ float2 prolong_elem(int nf1, int nf2, int nc1, int nc2, int nc3,
@@ -281,19 +332,27 @@ __global__ void k_high_pass(int n1, int n2, int n3, int ncomp, const float2* __r
 }
 
 // Fused end of the two-level apply: G = prolong(Fc) + high_pass(Ff) on the
-// fine half spectrum. One CTA per (component, k1, k2) row, threads along k3:
-// no index division at all.
+// fine half spectrum, flat over the elements (a CTA per n3/2 + 1 row left
+// most threads idle on the odd tail: 170 us -> memory speed at 256^3).
 __global__ void k_prolong_plus_hp(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3,
                                   const float2* __restrict__ Fc, const float2* __restrict__ Ff,
-                                  float2* __restrict__ G, float scale_p, float scale_h) {
+                                  float2* __restrict__ G, float scale_p, float scale_h,
+                                  float beta, int order) {
   const int hf = nf3 / 2 + 1, hc = nc3 / 2 + 1;
-  const int k2 = blockIdx.x, c = blockIdx.y / nf1, k1 = blockIdx.y - c * nf1;
   const size_t ncf = size_t(nf1) * nf2 * hf, ncc = size_t(nc1) * nc2 * hc;
-  const size_t row = size_t(c) * ncf + (size_t(k1) * nf2 + k2) * hf;
-  for (int k3 = threadIdx.x; k3 < hf; k3 += blockDim.x) {
+  const unsigned total = 3u * unsigned(ncf);
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int c = int(e / unsigned(ncf));
+    const unsigned r = e - unsigned(c) * unsigned(ncf);
+    int k1, k2, k3;
+    split3(r, unsigned(hf), unsigned(nf2), k1, k2, k3);
     const float2 a = prolong_elem(nf1, nf2, nc1, nc2, nc3, Fc + c * ncc, k1, k2, k3, scale_p);
-    const float2 b = high_pass_elem(nf1, nf2, nf3, Ff + c * ncf, k1, k2, k3, scale_h);
-    G[row + k3] = make_float2(a.x + b.x, a.y + b.y);
+    // high pass of InvA F: the alias partners it pairs share |k|
+    const int nu1 = k1 <= nf1 / 2 ? k1 : k1 - nf1, nu2 = k2 <= nf2 / 2 ? k2 : k2 - nf2;
+    const float hs = scale_h * inv_symbol(nu1, nu2, k3, beta, order);
+    const float2 b = high_pass_elem(nf1, nf2, nf3, Ff + c * ncf, k1, k2, k3, hs);
+    G[e] = make_float2(a.x + b.x, a.y + b.y);
   }
 }
 
@@ -361,7 +420,7 @@ void fft_inverse(vreg_ctx ctx, const Slab& s, int ncomp, float2* F, float* f) {
 void apply_symbol(vreg_ctx ctx, const SpecDesc& d, int ncomp, float2* F, double beta, bool inverse,
                   bool unit_zero, double scale) {
   Timed t(ctx, T_FFT, "spec_symbol");
-  k_symbol<<<dim3(unsigned(d.n2l), unsigned(ncomp * d.n1)), 128, 0, ctx->stream>>>(
+  k_symbol<<<blocks_for(size_t(ncomp) * d.nc, 256), 256, 0, ctx->stream>>>(
       d, ncomp, F, float(beta), inverse ? 1 : 0, unit_zero ? 1 : 0, float(scale), ctx->reg_order);
   count_launch(ctx);
   check_launch();
@@ -558,10 +617,11 @@ int vreg_fft_forward(vreg_ctx ctx, const vreg_grid* g, const float* f, float* ou
 
 // Fused fine-grid work of the two-level preconditioner (precond.hpp:143-160)
 // on one rank: one forward transform of r and one inverse for the result.
-//   begin: F = R2C(r); rc = C2R_c(restrict(F)); F *= 1/(beta |k|^2) (the
-//          spectrum of InvA r, zero mode 1/beta); sc = C2R_c(restrict(F));
+//   begin: F = R2C(r); one restriction pass gives restrict(F) and
+//          restrict(InvA F) = InvA_c restrict(F); rc, sc = C2R_c of both.
 //          F is kept for the end.
-//   end:   out = C2R(prolong(R2C_c(sc)) + high_pass(F)).
+//   end:   out = C2R(prolong(R2C_c(sc)) + high_pass(InvA F)), the symbol
+//          applied inside the high pass.
 int vreg_two_level_begin(vreg_ctx ctx, const vreg_grid* g, const float* r3, double beta_pc,
                          float* rc3, float* sc3) {
   return guard([&] {
@@ -573,19 +633,16 @@ int vreg_two_level_begin(vreg_ctx ctx, const vreg_grid* g, const float* r3, doub
     const SpecDesc df = spec_desc(ctx, s), dc = spec_desc(ctx, sc);
     float2* F = spec_buffer(ctx, df, 3, "tl_F");
     float2* Fc = spec_buffer(ctx, dc, 3, "tl_Fc");
+    float2* Fs = spec_buffer(ctx, dc, 3, "tl_Fs");
     fft_forward(ctx, s, 3, r3, F);
     const float rs = float(1.0 / double(s.global()));
-    k_restrict<<<blocks_for(dc.nc * 3, kT), kT, 0, ctx->stream>>>(s.n1, s.n2, s.n3, sc.n1, sc.n2,
-                                                                 sc.n3, 3, F, Fc, rs);
+    k_restrict_pair<<<blocks_for(dc.nc * 3, kT), kT, 0, ctx->stream>>>(
+        s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, F, Fc, Fs, rs, float(beta_pc), ctx->reg_order);
     count_launch(ctx);
     check_launch();
     fft_inverse(ctx, sc, 3, Fc, rc3);
-    apply_symbol(ctx, df, 3, F, beta_pc, true, true, 1.0);
-    k_restrict<<<blocks_for(dc.nc * 3, kT), kT, 0, ctx->stream>>>(s.n1, s.n2, s.n3, sc.n1, sc.n2,
-                                                                 sc.n3, 3, F, Fc, rs);
-    count_launch(ctx);
-    check_launch();
-    fft_inverse(ctx, sc, 3, Fc, sc3);
+    fft_inverse(ctx, sc, 3, Fs, sc3);
+    ctx->tl_beta = beta_pc;  // F stays the spectrum of r; the end applies InvA to it
   });
 }
 
@@ -600,9 +657,9 @@ int vreg_two_level_end(vreg_ctx ctx, const vreg_grid* g, const float* sc3, float
     float2* Fc = spec_buffer(ctx, dc, 3, "tl_Fc");
     float2* G = spec_buffer(ctx, df, 3, "tl_G");
     fft_forward(ctx, sc, 3, sc3, Fc);
-    k_prolong_plus_hp<<<dim3(unsigned(s.n2), unsigned(3 * s.n1)), 128, 0, ctx->stream>>>(
+    k_prolong_plus_hp<<<blocks_for(df.nc * 3, kT), kT, 0, ctx->stream>>>(
         s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, Fc, F, G, float(1.0 / double(sc.global())),
-        float(1.0 / double(s.global())));
+        float(1.0 / double(s.global())), float(ctx->tl_beta), ctx->reg_order);
     count_launch(ctx);
     check_launch();
     fft_inverse(ctx, s, 3, G, out3);

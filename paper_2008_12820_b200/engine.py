@@ -80,10 +80,13 @@ class Context:
         check(lib().vreg_slab(self.h, C.byref(g), C.byref(n1l), C.byref(off)))
         return n1l.value, off.value
 
-    def field(self, g, ncomp=1):
+    def field(self, g, ncomp=1, zero=True):
+        """This rank's slab of a device field (zero=False: uninitialised, for
+        outputs the library overwrites)."""
         n1l, _ = self.slab(g)
         shape = (n1l, g.n2, g.n3) if ncomp == 1 else (ncomp, n1l, g.n2, g.n3)
-        return torch.zeros(shape, dtype=torch.float32, device=f"cuda:{self.device}")
+        alloc = torch.zeros if zero else torch.empty
+        return alloc(shape, dtype=torch.float32, device=f"cuda:{self.device}")
 
     def to_global(self, g, f):
         """Global field on the host (numpy float32), slabs gathered over ranks."""

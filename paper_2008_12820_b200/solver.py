@@ -139,8 +139,8 @@ class Solver:
         except Exception:
             pass
 
-    def field(self, ncomp=1):
-        return self.ctx.field(self.grid, ncomp)
+    def field(self, ncomp=1, zero=True):
+        return self.ctx.field(self.grid, ncomp, zero)
 
     def set_images(self, m0, m1):
         check(lib().vreg_solver_set_images(self.h, _p(m0), _p(m1)))
@@ -162,12 +162,12 @@ class Solver:
         return dict(total=J[0], mismatch=J[1], regularization=J[2], div_penalty=J[3])
 
     def gradient(self):
-        g = self.field(3)
+        g = self.field(3, zero=False)
         check(lib().vreg_solver_gradient(self.h, _p(g)))
         return g
 
     def matvec(self, vt, out=None):
-        out = self.field(3) if out is None else out
+        out = self.field(3, zero=False) if out is None else out
         check(lib().vreg_solver_matvec(self.h, _p(vt), _p(out)))
         return out
 
@@ -191,7 +191,7 @@ class Solver:
         check(lib().vreg_solver_wait(self.h))
 
     def precond(self, kind, r, eps_k):
-        out = self.field(3)
+        out = self.field(3, zero=False)
         st = (C.c_uint64 * 4)()
         check(lib().vreg_solver_precond(self.h, PRECOND[kind], _p(r), eps_k, _p(out), st))
         return out, dict(inva=st[0], h0=st[1], inner=st[2], capped=bool(st[3]))
