@@ -1,12 +1,17 @@
 // The Gauss-Newton Hessian matvec on device (proj/include/vreg/optim.hpp:115-137,
 // HessianAdjoint::Transpose with the gradient cache on):
 //
-//   inc state   : nt fused gather steps (linearity: I[m~] - dt/2 I[u] = I[w])
-//   transpose   : nt scatter sweeps psi_{t-1} = I^T psi_t
-//   regulariser : R2C(vt) -> beta |k|^2 / N -> C2R   (cuFFT, timed as fft)
+//   pre-pass    : w_0 and u_t = vt . grad m_t for all t (k_inc_u)
+//   inc state   : nt fused gather steps (linearity: I[m~] - dt/2 I[u] = I[w]),
+//                 the TMA-fed pipeline of sl_pipe.cuh
+//   transpose   : nt scatter sweeps psi_{t-1} = I^T psi_t (sl_tile.cuh)
+//   regulariser : beta (D_3 + D_2 + D_1) vt as three separable 1-D spectral
+//                 passes (spec_axis.cu, H1; x1 pass over the slab transpose on
+//                 several GPUs), else R2C -> symbol -> C2R through cuFFT
+//                 (H2 or axis sizes the in-register FFT lacks); timed as fft
 //   assembly    : out = sum_{t=nt..0} w_t psi_t grad m_t + beta A vt, one pass
 //
-// 2 nt + 2 of our kernels + 2 batched cuFFT calls per matvec.
+// 2 nt + 5 of our kernels per matvec on one GPU, no host synchronisation.
 #include <cstdlib>
 #include "common.cuh"
 
