@@ -130,6 +130,7 @@ struct vreg_ctx_s {
   // the reference's spectral.cpp:61-63), 2 = H2 (|k|^4, B200 extension)
   int reg_order = 1;
   double tl_beta = 0;  // beta_pc of the last two-level begin (read by its end)
+  bool pipe_dynamic = false;  // next gather-pipe launches take tiles from a ticket counter
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;
   // regulariser x2-slab transposes by copy engine into the peers' buffers
@@ -221,6 +222,33 @@ inline void count_launch(vreg_ctx ctx, uint64_t n = 1) { ctx->launches += n; }
 void smem_optin(const void* kernel, int bytes);
 
 inline void check_launch() { VB_CUDA(cudaGetLastError()); }
+
+// Division by a runtime-invariant divisor as a multiply-high and shift
+// (round-up reciprocal, exact for dividends < 2^31): the flat spectral
+// kernels split element indices with it instead of 32-bit IDIV sequences.
+struct FastDiv {
+  unsigned d = 1, m = 0;
+  int sh = 0;
+  FastDiv() = default;
+  explicit FastDiv(unsigned dv) : d(dv) {
+    if (d <= 1) return;
+    int l = 0;
+    while ((1u << l) < d) ++l;  // ceil log2 d
+    const int p = 31 + l;
+    m = unsigned(((1ull << p) + d - 1) / d);
+    sh = p - 32;
+  }
+#ifdef __CUDACC__
+  __device__ __forceinline__ unsigned div(unsigned n) const {
+    return d == 1 ? n : (__umulhi(n, m) >> sh);
+  }
+  __device__ __forceinline__ unsigned divmod(unsigned n, unsigned& r) const {
+    const unsigned q = div(n);
+    r = n - q * d;
+    return q;
+  }
+#endif
+};
 
 inline unsigned blocks_for(size_t n, unsigned threads, unsigned cap = 148u * 32u) {
   size_t b = (n + threads - 1) / threads;

@@ -9,6 +9,8 @@
 #include <map>
 #include <mutex>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 
 namespace vb {
@@ -122,7 +124,16 @@ FftPlans& fft_plans(vreg_ctx ctx, int n1, int n2, int n3, int batch) {
   return ctx->plans.emplace(key, p).first->second;
 }
 
+namespace {
+const char* const kCatNames[T_COUNT] = {"fft",          "fd",           "sl",
+                                        "ghost_comm",   "interp_comm",  "scatter_comm",
+                                        "scatter_buffer", "transpose_comm"};
+}  // namespace
+
+// Every timed kernel group is also an NVTX range (ranges per
+// engine call next to the CUDA-event timers), visible to nsys / ncu --nvtx.
 Timed::Timed(vreg_ctx ctx, int cat, const char* name) : ctx_(ctx), cat_(cat), name_(name) {
+  nvtxRangePushA(name ? name : (cat >= 0 && cat < T_COUNT ? kCatNames[cat] : "vreg"));
   if (!ctx_->timers_on) return;
   if (ctx_->event_pool.empty()) {
     cudaEvent_t e;
@@ -135,6 +146,7 @@ Timed::Timed(vreg_ctx ctx, int cat, const char* name) : ctx_(ctx), cat_(cat), na
 }
 
 Timed::~Timed() {
+  nvtxRangePop();
   if (!a_) return;
   cudaEvent_t b;
   if (ctx_->event_pool.empty()) {
@@ -152,7 +164,7 @@ void resolve_timers(vreg_ctx ctx) {
   for (auto& p : ctx->pending) {
     float ms = 0.f;
     VB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
-    ctx->timer_acc[p.cat] += double(ms) * 1e-3;
+    if (p.cat >= 0) ctx->timer_acc[p.cat] += double(ms) * 1e-3;  // cat < 0: named only
     if (p.name) {
       auto& st = ctx->kstats[p.name];
       st.first += 1;

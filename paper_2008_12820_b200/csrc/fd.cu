@@ -9,6 +9,7 @@
 // Tiling: see the x1-marching kernels below (register window along x1,
 // double-buffered shared tile with the x2/x3 halo of 4).
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -16,7 +17,7 @@ namespace vb {
 
 namespace {
 
-constexpr int TX = 32, TY = 8, H = 4;
+constexpr int TX = 32, H = 4;
 
 // Paired 8th-order first-derivative weights c_j, j = 1..4, unit spacing: the
 // antisymmetric half of the 9-point Fornberg stencil the reference builds in
@@ -56,10 +57,6 @@ __device__ __forceinline__ const float* fd_plane(const float* f, const float* lo
 // fresh global load. Each input element is read from HBM about once; no
 // integer division is left in the loop. Same paired sums in the same order as
 // the per-plane formulation: bitwise identical results.
-#ifndef VB_FD_CH
-#define VB_FD_CH 16
-#endif
-constexpr int FD_CH = VB_FD_CH;  // planes per CTA
 constexpr int FD_RING = 3;  // shared tiles in flight
 constexpr int TW = TX + 2 * H;
 
@@ -69,6 +66,7 @@ __device__ __forceinline__ int wrap_fd(int x, int n) { return x < 0 ? x + n : (x
 __device__ __forceinline__ int wrap_col(int x, int n) {
   return n >= TW ? wrap_fd(x, n) : ((x % n) + n) % n;
 }
+template <int TY>
 __device__ __forceinline__ int wrap_row(int x, int n) {
   return n >= TY + 2 * H ? wrap_fd(x, n) : ((x % n) + n) % n;
 }
@@ -89,6 +87,7 @@ __device__ __forceinline__ void fd_wait() {
 
 // Issue the tile + halo of plane P (rows j0-H .. j0+TY+H-1, columns k0-H ..
 // k0+TX+H-1, periodic) into t: 16-byte chunks when n3 % 4 == 0.
+template <int TY>
 __device__ __forceinline__ void stage_async(float (*t)[TW], const float* P, int j0, int k0,
                                             const FdGeo& g) {
   const int tid = threadIdx.y * TX + threadIdx.x;
@@ -96,19 +95,19 @@ __device__ __forceinline__ void stage_async(float (*t)[TW], const float* P, int 
     constexpr int CH = TW / 4;  // 10 chunks per row
     for (int c = tid; c < (TY + 2 * H) * CH; c += TX * TY) {
       const int y = c / CH, x4 = c - y * CH;
-      const float* R = P + size_t(wrap_row(j0 + y - H, g.n2)) * g.n3;
+      const float* R = P + size_t(wrap_row<TY>(j0 + y - H, g.n2)) * g.n3;
       fd_cp16(&t[y][4 * x4], R + wrap_col(k0 - H + 4 * x4, g.n3));
     }
   } else {
     for (int c = tid; c < (TY + 2 * H) * TW; c += TX * TY) {
       const int y = c / TW, x = c - y * TW;
-      const float* R = P + size_t(wrap_row(j0 + y - H, g.n2)) * g.n3;
+      const float* R = P + size_t(wrap_row<TY>(j0 + y - H, g.n2)) * g.n3;
       fd_cp4(&t[y][x], R + wrap_col(k0 - H + x, g.n3));
     }
   }
 }
 
-template <bool DIST, bool DIV>
+template <bool DIST, bool DIV, int TY, int FD_CH>
 __global__ void __launch_bounds__(TX* TY) k_fd_m(FdGeo g, const float* __restrict__ f,
                                                  const float* __restrict__ lo,
                                                  const float* __restrict__ hi, FdW w, float h1,
@@ -134,7 +133,7 @@ __global__ void __launch_bounds__(TX* TY) k_fd_m(FdGeo g, const float* __restric
   for (int d = 0; d < 2; ++d) {
     if (i0 + d < i1)
 #pragma unroll
-      for (int r = 0; r < NR; ++r) stage_async(t[r][d], ring_src(r, i0 + d), j0, k0, g);
+      for (int r = 0; r < NR; ++r) stage_async<TY>(t[r][d], ring_src(r, i0 + d), j0, k0, g);
     fd_commit();
   }
   float win[2 * H + 1];
@@ -149,7 +148,7 @@ __global__ void __launch_bounds__(TX* TY) k_fd_m(FdGeo g, const float* __restric
     if (i + 2 < i1)
 #pragma unroll
       for (int r = 0; r < NR; ++r)
-        stage_async(t[r][(i + 2 - i0) % FD_RING], ring_src(r, i + 2), j0, k0, g);
+        stage_async<TY>(t[r][(i + 2 - i0) % FD_RING], ring_src(r, i + 2), j0, k0, g);
     fd_commit();
     const float nxt2 =
         (valid && i + 2 < i1) ? __ldg(fd_plane<DIST>(f, lo, hi, i + H + 2, g) + off) : 0.f;
@@ -181,6 +180,18 @@ __global__ void __launch_bounds__(TX* TY) k_fd_m(FdGeo g, const float* __restric
     nxt = nxt2;
   }
   fd_wait<0>();
+}
+
+// Launch k_fd_m: 32 x 8 columns, 16 planes per CTA (measured best of
+// 4/8/16 rows x 16/32/64 planes at 256^3).
+template <bool DIST, bool DIV>
+void launch_fd(vreg_ctx ctx, const Slab& s, const FdGeo& g, const float* f, const float* lo,
+               const float* hi, float h1, float h2, float h3, float* out) {
+  constexpr int ty = 8, ch = 16;
+  const dim3 grid((s.n3 + TX - 1) / TX, (s.n2 + ty - 1) / ty, (s.n1l + ch - 1) / ch),
+      block(TX, ty);
+  k_fd_m<DIST, DIV, ty, ch><<<grid, block, 0, ctx->stream>>>(g, f, lo, hi, fd_weights(), h1, h2,
+                                                             h3, out);
 }
 
 FdGeo fd_geo(const Slab& s) {
@@ -217,15 +228,11 @@ int vreg_fd_grad(vreg_ctx ctx, const vreg_grid* gr, const float* f, float* out3)
     }
     Timed t(ctx, T_FD, "fd_grad");
     const FdGeo g = fd_geo(s);
-    const dim3 grid((s.n3 + TX - 1) / TX, (s.n2 + TY - 1) / TY, (s.n1l + FD_CH - 1) / FD_CH),
-        block(TX, TY);
     const float h1 = float(1.0 / s.h(0)), h2 = float(1.0 / s.h(1)), h3 = float(1.0 / s.h(2));
     if (dist)
-      k_fd_m<true, false><<<grid, block, 0, ctx->stream>>>(g, f, gh.lo, gh.hi, fd_weights(), h1,
-                                                         h2, h3, out3);
+      launch_fd<true, false>(ctx, s, g, f, gh.lo, gh.hi, h1, h2, h3, out3);
     else
-      k_fd_m<false, false><<<grid, block, 0, ctx->stream>>>(g, f, nullptr, nullptr, fd_weights(),
-                                                          h1, h2, h3, out3);
+      launch_fd<false, false>(ctx, s, g, f, nullptr, nullptr, h1, h2, h3, out3);
     count_launch(ctx);
     check_launch();
   });
@@ -243,15 +250,11 @@ int vreg_fd_div(vreg_ctx ctx, const vreg_grid* gr, const float* v3, float* out) 
     }
     Timed t(ctx, T_FD, "fd_div");
     const FdGeo g = fd_geo(s);
-    const dim3 grid((s.n3 + TX - 1) / TX, (s.n2 + TY - 1) / TY, (s.n1l + FD_CH - 1) / FD_CH),
-        block(TX, TY);
     const float h1 = float(1.0 / s.h(0)), h2 = float(1.0 / s.h(1)), h3 = float(1.0 / s.h(2));
     if (dist)
-      k_fd_m<true, true><<<grid, block, 0, ctx->stream>>>(g, v3, gh.lo, gh.hi, fd_weights(), h1,
-                                                        h2, h3, out);
+      launch_fd<true, true>(ctx, s, g, v3, gh.lo, gh.hi, h1, h2, h3, out);
     else
-      k_fd_m<false, true><<<grid, block, 0, ctx->stream>>>(g, v3, nullptr, nullptr, fd_weights(),
-                                                         h1, h2, h3, out);
+      launch_fd<false, true>(ctx, s, g, v3, nullptr, nullptr, h1, h2, h3, out);
     count_launch(ctx);
     check_launch();
   });

@@ -313,7 +313,10 @@ class DevicePrecond {
       // s0 = InvA_pc r, then PCG on H0 s = r with InvA_pc (precond.hpp:104-131)
       const vreg_grid g = eng_->vg();
       check(vreg_inv_regop(ctx, &g, r, beta_pc_, z));
-      inner(*eng_, *gm_).solve(op_h0(*eng_, *gm_), op_inv(*eng_), r, z, tol, cap_, true, acc_);
+      if (split_h0())
+        inner(*eng_, *gm_).solve_h0(gm_->data(), op_inv(*eng_), r, z, tol, cap_, acc_);
+      else
+        inner(*eng_, *gm_).solve(op_h0(*eng_, *gm_), op_inv(*eng_), r, z, tol, cap_, true, acc_);
       return;
     }
     // two-level: restrictions of r and InvA_pc r from one forward transform,
@@ -326,23 +329,35 @@ class DevicePrecond {
     const vreg_grid g = eng_->vg();
     if (eng_->workers() == 1) {
       check(vreg_two_level_begin(ctx, &g, r, beta_pc_, rc_->data(), sc_->data()));
-    } else {  // slab-distributed spectral ops, unfused
+    } else {
+      // slab-distributed: restrict(InvA_f r) = InvA_c restrict(r) mode by
+      // mode, so high_pass(InvA_f r) = InvA_f r - prolong(s_c0) with the
+      // coarse start s_c0 = InvA_c r_c, and the apply is
+      // InvA_f r + prolong(s_c - s_c0): one fine restriction and one
+      // prolongation instead of three and two (precond.hpp:133-162)
       if (!tmp_) {
         tmp_.emplace(eng_->make_vfield());
-        hp_.emplace(eng_->make_vfield());
+        sc0_.emplace(ce.make_vfield());
       }
+      const vreg_grid gc = ce.vg();
       check(vreg_inv_regop(ctx, &g, r, beta_pc_, tmp_->data()));
       check(vreg_restrict(ctx, &g, 3, r, rc_->data()));
-      check(vreg_restrict(ctx, &g, 3, tmp_->data(), sc_->data()));
+      check(vreg_inv_regop(ctx, &gc, rc_->data(), beta_pc_, sc_->data()));
+      check(vreg_copy(ctx, &gc, 3, sc_->data(), sc0_->data()));
     }
-    inner(ce, *gm_c_).solve(op_h0(ce, *gm_c_), op_inv(ce), rc_->data(), sc_->data(), tol, cap_,
-                            true, acc_);
+    if (split_h0())
+      inner(ce, *gm_c_).solve_h0(gm_c_->data(), op_inv(ce), rc_->data(), sc_->data(), tol, cap_,
+                                 acc_);
+    else
+      inner(ce, *gm_c_).solve(op_h0(ce, *gm_c_), op_inv(ce), rc_->data(), sc_->data(), tol,
+                              cap_, true, acc_);
     if (eng_->workers() == 1) {
       check(vreg_two_level_end(ctx, &g, sc_->data(), z));
     } else {
+      const vreg_grid gc = ce.vg();
+      check(vreg_axpy(ctx, &gc, 3, -1.0, sc0_->data(), sc_->data()));
       check(vreg_prolong(ctx, &g, 3, sc_->data(), z));
-      check(vreg_high_pass(ctx, &g, 3, tmp_->data(), hp_->data()));
-      check(vreg_axpy(ctx, &g, 3, 1.0, hp_->data(), z));
+      check(vreg_axpy(ctx, &g, 3, 1.0, tmp_->data(), z));
     }
   }
 
@@ -439,6 +454,15 @@ class DevicePrecond {
   }
 
  private:
+  // the inner H0 solves run split (one spectral solve per iteration,
+  // Krylov::solve_h0); VREG_H0_SPLIT=0 applies H0 and InvA as two operators
+  static bool split_h0() {
+    static const bool on = [] {
+      const char* e = std::getenv("VREG_H0_SPLIT");
+      return !(e && e[0] == '0');
+    }();
+    return on;
+  }
   static bool graph_ok() {
     const char* e = std::getenv("VREG_PCG_GRAPH");
     return !(e && e[0] == '0');
@@ -472,7 +496,7 @@ class DevicePrecond {
   PrecondKind kind_;
   Real beta_, beta_pc_, eps_h0_;
   int cap_;
-  std::optional<DVField> gm_, gm_c_, rc_, sc_, tmp_, hp_, gin_, gout_;
+  std::optional<DVField> gm_, gm_c_, rc_, sc_, sc0_, tmp_, gin_, gout_;
   std::unique_ptr<vb::Krylov> kf_, kc_;
   unsigned long long* acc_ = nullptr;
   cudaGraphExec_t graph_ = nullptr;

@@ -66,6 +66,14 @@ class Krylov {
   KrylovStats solve(const KrylovOp& A, const KrylovOp& M, const float* b, float* x, double tol,
                     int max_it, bool x0, unsigned long long* acc = nullptr, bool graph = true);
 
+  // The H0 inner solve of precond.hpp:104-162 with the operator split
+  // H0 = B + G (B = beta_pc A, G s = gm (gm . s), pointwise) and M = B^-1:
+  // x holds x0 = M b on entry (the reference's initial guess), so r0 = -G x0;
+  // y = B p and z = M r are carried by recurrences and an iteration applies
+  // M once (to G p) instead of M and B. fp32 iterates only.
+  KrylovStats solve_h0(const float* gm, const KrylovOp& M, const float* b, float* x, double tol,
+                       int max_it, unsigned long long* acc = nullptr, bool graph = true);
+
   const Slab& slab() const { return s_; }
   bool fp64() const { return fp64_; }
 
@@ -75,7 +83,7 @@ class Krylov {
   void issue_body(const KrylovOp& A, const KrylovOp& M, unsigned long long cond);
   void issue_fold(int mode, unsigned long long cond);
   void issue_finish(float* x, unsigned long long* acc);
-  void dot(const void* a, const float* b32);
+  void dot(const void* a, const float* b32, double* dst = nullptr);
   KrylovStats read_stats();
   void capture_loop(const KrylovOp& A, const KrylovOp& M, bool nested);
 
@@ -92,6 +100,10 @@ class Krylov {
   int hist_cap_ = 0;
   KrylovState* h_st_ = nullptr;  // pinned
   cudaStream_t cap_stream_ = nullptr;
+  // split H0 solve (solve_h0): gradient field, M, and the y / G p / M G p vectors
+  const float* h0g_ = nullptr;
+  const KrylovOp* h0m_ = nullptr;
+  float *y_ = nullptr, *gp_ = nullptr, *mg_ = nullptr;
 };
 
 }  // namespace vb

@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_chars_tile(
 // order, so the last bits can differ between runs (VREG_DETERMINISTIC=1 /
 // vreg_ctx_set_deterministic selects the fixed-point variant below).
 template <int DEG, bool DIST>
-__global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_scatter_tile_fp(Geo g, DstField<DIST> dst,
+__global__ void __launch_bounds__(TILE_THREADS, DIST ? 2 : TILE_MIN_BLOCKS) k_scatter_tile_fp(Geo g, DstField<DIST> dst,
                                                                   const int* __restrict__ boxes,
                                                                   const float* __restrict__ D,
                                                                   const float* __restrict__ z,
@@ -619,16 +619,32 @@ void gather_tiles(vreg_ctx ctx, const Slab& s, const float* f, int G, bool dist,
     launch(kAllLayers, ls.ntz);
     return;
   }
+  // the halo exchange and then the boundary layers run on the comm stream,
+  // next to the interior sweep: the boundary sweep (dynamically scheduled)
+  // starts on the SMs the interior leaves free and fills the ones its CTAs
+  // release, instead of running alone after it
   VB_CUDA(cudaEventRecord(ctx->ev_c0, ctx->stream));
   VB_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_c0, 0));
   {
     OnStream os(ctx, ctx->comm_stream);
     gh = halo_exchange(ctx, s, f, G, "sl_ghost", T_INTERP_COMM, C_GHOST_INTERP);
-    VB_CUDA(cudaEventRecord(ctx->ev_c1, ctx->stream));
+    Timed tb(ctx, -1, "sl_gather_boundary");
+    ctx->pipe_dynamic = true;
+    try {
+      launch(TileZ{0, ls.zb, ls.ntz - ls.zb}, 2 * ls.zb);
+    } catch (...) {
+      ctx->pipe_dynamic = false;
+      throw;
+    }
+    ctx->pipe_dynamic = false;
   }
-  launch(TileZ{ls.zb, 1 << 30, 0}, ls.ntz - 2 * ls.zb);
+  VB_CUDA(cudaEventRecord(ctx->ev_c1, ctx->comm_stream));
+  {
+    Timed ti(ctx, -1, "sl_gather_interior");
+    launch(TileZ{ls.zb, 1 << 30, 0}, ls.ntz - 2 * ls.zb);
+  }
+  Timed tw(ctx, -1, "sl_gather_boundary_wait");
   VB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_c1, 0));
-  launch(TileZ{0, ls.zb, ls.ntz - ls.zb}, 2 * ls.zb);
 }
 
 // Tile scatter on several ranks: the boundary bands (the only tiles that
@@ -647,16 +663,25 @@ void scatter_tiles(vreg_ctx ctx, const Slab& s, const GhostAcc& acc, float* out,
     halo_reverse_add(ctx, s, acc, out, "sl_gacc", as_int);
     return;
   }
-  launch(TileZ{0, ls.zb, ls.ntz - ls.zb}, 2 * ls.zb);
+  // boundary bands and their reverse exchange on the (high-priority) comm
+  // stream, beside the interior sweep: both only add into out (atomics), and
+  // the boundary's last partial wave no longer runs alone
   VB_CUDA(cudaEventRecord(ctx->ev_c0, ctx->stream));
   VB_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_c0, 0));
   RevHalo r;
   {
     OnStream os(ctx, ctx->comm_stream);
+    {
+      Timed tb(ctx, -1, "sl_scatter_boundary");
+      launch(TileZ{0, ls.zb, ls.ntz - ls.zb}, 2 * ls.zb);
+    }
     r = halo_reverse_send(ctx, s, acc, "sl_gacc");
     VB_CUDA(cudaEventRecord(ctx->ev_c1, ctx->stream));
   }
-  launch(TileZ{ls.zb, 1 << 30, 0}, ls.ntz - 2 * ls.zb);
+  {
+    Timed ti(ctx, -1, "sl_scatter_interior");
+    launch(TileZ{ls.zb, 1 << 30, 0}, ls.ntz - 2 * ls.zb);
+  }
   VB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_c1, 0));
   halo_reverse_finish(ctx, s, r, out, as_int);
 }
@@ -785,6 +810,18 @@ inline PipeTiles pipe_tiles(const Slab& s, int nz) {
   return t;
 }
 
+// Tile ticket counters of the pipeline launches ({next ticket, CTAs done},
+// zero between launches: the last CTA of a launch rewinds its pair). A ring
+// of pairs, so launches in flight on different streams never share one.
+constexpr int kSchedSlots = 64;
+int* pipe_sched(vreg_ctx ctx) {
+  const bool fresh = ctx->ws.find("pipe_sched") == ctx->ws.end();
+  int* base = static_cast<int*>(workspace(ctx, "pipe_sched", 2 * kSchedSlots * sizeof(int)));
+  if (fresh) VB_CUDA(cudaMemsetAsync(base, 0, 2 * kSchedSlots * sizeof(int), ctx->stream));
+  static thread_local unsigned slot = 0;
+  return base + 2 * (slot++ % kSchedSlots);
+}
+
 template <class Kern>
 inline Kern pipe_kernel(Kern k) {
   smem_optin(reinterpret_cast<const void*>(k), int(PIPE_SMEM));
@@ -873,12 +910,21 @@ void gather_pipe(vreg_ctx ctx, const Slab& s, int degree, bool dist, const float
   const CUtensorMap tmD = tmap_planes(disp3, s, 3 * s.n1l);
   const CUtensorMap tmA = aux ? tmap_planes(aux, s, s.n1l) : tmD;
   const PipeTiles pt = pipe_tiles(s, nz);
-  const unsigned grid = unsigned(std::min(pt.n, sm_count(ctx)));
+  // One persistent CTA per SM holds its SM for the whole sweep, so on
+  // several GPUs a few SMs stay free for the NCCL kernels of the halo
+  // exchanges that overlap the interior layers (VREG_PIPE_RESERVE SMs)
+  static const int reserve = [] {
+    const char* e = std::getenv("VREG_PIPE_RESERVE");
+    return e ? std::max(0, std::atoi(e)) : 8;
+  }();
+  const int ctas = ctx->nranks > 1 ? std::max(1, sm_count(ctx) - reserve) : sm_count(ctx);
+  const unsigned grid = unsigned(std::min(pt.n, ctas));
+  int* sched = ctx->pipe_dynamic ? pipe_sched(ctx) : nullptr;
   SL_DISPATCH(degree, dist,
               (pipe_kernel(k_gather_pipe<DEG, DIST, MODE>)<<<grid, PIPE_THREADS, PIPE_SMEM,
                                                              ctx->stream>>>(
                   g, src_of<DIST>(f, gh), boxes, tmD, tmA, aux ? 1 : 0, out, half, last, mt_out,
-                  zm, pt)));
+                  zm, pt, sched)));
 }
 
 struct CharsInfo {

@@ -256,8 +256,9 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1)
     k_gather_pipe(Geo g, SrcField<DIST> src, const int* __restrict__ boxes,
                   const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmA,
                   int has_aux, float* __restrict__ out, float half, int last,
-                  float* __restrict__ mt_out, TileZ zm, PipeTiles pt) {
+                  float* __restrict__ mt_out, TileZ zm, PipeTiles pt, int* __restrict__ sched) {
   extern __shared__ __align__(128) float pipe_raw[];
+  __shared__ int next_tile;
   __shared__ __align__(8) uint64_t full[PIPE_STAGES], empty[PIPE_STAGES];
   __shared__ PipeHdr hdr[PIPE_STAGES];
   __shared__ const float* rows[PIPE_STAGES][PIPE_BOX_ROWS];
@@ -274,22 +275,51 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1)
   }
   __syncthreads();
   if (warp >= PIPE_CONS_WARPS) {  // ---- producer group
-    int it = 0;
-    for (int tile = blockIdx.x; tile < pt.n; tile += gridDim.x, ++it) {
+    // static round robin, or (sched != nullptr) tiles taken from a global
+    // ticket counter, so CTAs that start late -- their SMs still busy with
+    // another kernel -- take fewer tiles instead of delaying the sweep (the
+    // multi-rank boundary layers, launched while the interior sweep drains)
+    const int t = threadIdx.x - PIPE_CONS;
+    for (int it = 0;; ++it) {
       const int s = it % PIPE_STAGES;
       mbar_wait(&empty[s], ((it / PIPE_STAGES) & 1) ^ 1);
+      int tile;
+      if (sched) {
+        if (t == 0) next_tile = atomicAdd(&sched[0], 1);
+        asm volatile("bar.sync 1, %0;" ::"n"(PIPE_PROD) : "memory");
+        tile = next_tile;
+      } else {
+        tile = int(blockIdx.x) + it * int(gridDim.x);
+      }
+      if (tile >= pt.n) {  // sentinel stage: the consumers stop on it
+        if (t == 0) {
+          hdr[s].t[0] = -1;
+          mbar_expect_tx(&full[s], 0u);
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                         smem_addr(&full[s]))
+                     : "memory");
+        // the last CTA out rewinds the counter for the next launch
+        if (sched && t == 0) {
+          __threadfence();
+          if (atomicAdd(&sched[1], 1) == int(gridDim.x) - 1) {
+            atomicExch(&sched[0], 0);
+            atomicExch(&sched[1], 0);
+          }
+        }
+        return;
+      }
       pipe_produce<DIST>(g, src, boxes, &tmD, has_aux ? &tmA : nullptr, true, pt, zm, tile,
                          smem + s * PIPE_STAGE_WORDS, &hdr[s], rows[s], &full[s]);
     }
-    return;
   }
   // ---- consumers: thread = points (g1 + q1, g2 + q2, lane), q1, q2 in {0, 1}
   const int g1 = 2 * (warp >> 3), g2 = 2 * (warp & 7);
-  int it = 0;
-  for (int tile = blockIdx.x; tile < pt.n; tile += gridDim.x, ++it) {
+  for (int it = 0;; ++it) {
     const int s = it % PIPE_STAGES;
     mbar_wait(&full[s], (it / PIPE_STAGES) & 1);
     const PipeHdr h = hdr[s];
+    if (h.t[0] < 0) break;
     const float* st = smem + s * PIPE_STAGE_WORDS;
     const bool fits = h.ext[0] > 0;
     const int k = h.t[2] + lane;

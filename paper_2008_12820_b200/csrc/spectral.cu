@@ -22,7 +22,7 @@ struct SpecDesc {
   size_t nc;          // local complex elements per component
 };
 
-// 32-bit index arithmetic: a GPU's spectra stay below 2^32 elements, and
+// 32-bit index arithmetic: a GPU's spectra stay below 2^31 elements, and
 // 64-bit div/mod (~100 instructions each) dominated these streaming passes.
 __device__ __forceinline__ void spec_index(const SpecDesc& d, unsigned e, int& k1, int& k2, int& k3) {
   k3 = int(e % unsigned(d.h));
@@ -31,13 +31,21 @@ __device__ __forceinline__ void spec_index(const SpecDesc& d, unsigned e, int& k
   k1 = int(r / unsigned(d.n2l));
 }
 
-__device__ __forceinline__ void split3(unsigned r, unsigned h, unsigned n2, int& k1, int& k2,
-                                       int& k3) {
-  k3 = int(r % h);
-  const unsigned q = r / h;
-  k2 = int(q % n2);
-  k1 = int(q / n2);
-}
+// Flat element e of ncomp stacked half spectra [c][k1][k2][k3 < h]: the
+// component and wavenumbers by multiply-high divisions (FastDiv).
+struct Idx3 {
+  FastDiv h, n2, nc;
+  Idx3(unsigned hh, unsigned nn2, size_t ncc) : h(hh), n2(nn2), nc(unsigned(ncc)) {}
+  __device__ __forceinline__ int split(unsigned e, int& k1, int& k2, int& k3) const {
+    unsigned r, k3u, k2u;
+    const unsigned c = nc.divmod(e, r);
+    const unsigned q = h.divmod(r, k3u);
+    k1 = int(n2.divmod(q, k2u));
+    k2 = int(k2u);
+    k3 = int(k3u);
+    return int(c);
+  }
+};
 
 __device__ __forceinline__ float sfreq(int k, int n) { return float(k <= n / 2 ? k : k - n); }
 
@@ -48,17 +56,16 @@ constexpr unsigned kT = 256;
 // F *= scale * sym(k), sym = beta |k|^2 (zero mode: unit or 0) [regop] or
 // 1 / (beta |k|^2) (zero mode 1/beta) [inv_regop] (spectral.cpp:48-93);
 // order 2: |k|^4 (H2).
-__global__ void k_symbol(SpecDesc d, int ncomp, float2* __restrict__ F, float beta, int inverse,
-                         int unit_zero, float scale, int order) {
+__global__ void k_symbol(SpecDesc d, Idx3 ix, int ncomp, float2* __restrict__ F, float beta,
+                         int inverse, int unit_zero, float scale, int order) {
   // flat over every (component, k1, local k2, k3) element: one row of
   // n3/2 + 1 per CTA left most threads idle on the odd tail element
   const unsigned total = unsigned(ncomp) * unsigned(d.n1) * unsigned(d.n2l) * unsigned(d.h);
   const unsigned stride = gridDim.x * blockDim.x;
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const unsigned k3 = e % unsigned(d.h), row = e / unsigned(d.h);
-    const unsigned k2l = row % unsigned(d.n2l), k1 = (row / unsigned(d.n2l)) % unsigned(d.n1);
-    const float f1 = sfreq(int(k1), d.n1), f2 = sfreq(int(k2l) + d.k2off, d.n2),
-                f3 = float(k3);
+    int k1, k2l, k3;
+    ix.split(e, k1, k2l, k3);
+    const float f1 = sfreq(k1, d.n1), f2 = sfreq(k2l + d.k2off, d.n2), f3 = float(k3);
     float sym = f1 * f1 + f2 * f2 + f3 * f3;
     if (order == 2) sym *= sym;  // H2: |k|^4
     float m;
@@ -166,17 +173,15 @@ __device__ __forceinline__ int pmod(int a, int n) {
 
 // Coarse half spectrum from the fine one: partner sums on the coarse
 // Nyquist lines, times scale (spectral.cpp:149-174).
-__global__ void k_restrict(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3, int ncomp,
+__global__ void k_restrict(Idx3 ix, int nf1, int nf2, int nf3, int nc1, int nc2, int nc3, int ncomp,
                            const float2* __restrict__ Ff, float2* __restrict__ Fc, float scale) {
   const int hc = nc3 / 2 + 1, hf = nf3 / 2 + 1;
   const size_t ncc = size_t(nc1) * nc2 * hc, ncf = size_t(nf1) * nf2 * hf;
   const unsigned total = unsigned(ncc) * unsigned(ncomp);
   const unsigned stride = gridDim.x * blockDim.x;
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int c = int(e / unsigned(ncc));
-    const unsigned r = e - unsigned(c) * unsigned(ncc);
     int k1, k2, k3;
-    split3(r, unsigned(hc), unsigned(nc2), k1, k2, k3);
+    const int c = ix.split(e, k1, k2, k3);
     const int nu1 = k1 <= nc1 / 2 ? k1 : k1 - nc1;
     const int nu2 = k2 <= nc2 / 2 ? k2 : k2 - nc2;
     const int nu3 = k3;
@@ -212,7 +217,7 @@ __device__ __forceinline__ float inv_symbol(int nu1, int nu2, int nu3, float bet
 // spectrum: Fr = restrict(F) and Fs = restrict(InvA F). Restriction only
 // pairs alias partners of equal |k| (the coarse Nyquist lines), so
 // restrict(InvA F) = InvA_c restrict(F) mode by mode.
-__global__ void k_restrict_pair(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3,
+__global__ void k_restrict_pair(Idx3 ix, int nf1, int nf2, int nf3, int nc1, int nc2, int nc3,
                                 const float2* __restrict__ Ff, float2* __restrict__ Fr,
                                 float2* __restrict__ Fs, float scale, float beta, int order) {
   const int hc = nc3 / 2 + 1, hf = nf3 / 2 + 1;
@@ -220,10 +225,8 @@ __global__ void k_restrict_pair(int nf1, int nf2, int nf3, int nc1, int nc2, int
   const unsigned total = 3u * unsigned(ncc);
   const unsigned stride = gridDim.x * blockDim.x;
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int c = int(e / unsigned(ncc));
-    const unsigned r = e - unsigned(c) * unsigned(ncc);
     int k1, k2, k3;
-    split3(r, unsigned(hc), unsigned(nc2), k1, k2, k3);
+    const int c = ix.split(e, k1, k2, k3);
     const int nu1 = k1 <= nc1 / 2 ? k1 : k1 - nc1;
     const int nu2 = k2 <= nc2 / 2 ? k2 : k2 - nc2;
     const int nu3 = k3;
@@ -266,17 +269,15 @@ __device__ __forceinline__ float2 prolong_elem(int nf1, int nf2, int nc1, int nc
   return make_float2(0.f, 0.f);
 }
 
-__global__ void k_prolong(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3, int ncomp,
+__global__ void k_prolong(Idx3 ix, int nf1, int nf2, int nf3, int nc1, int nc2, int nc3, int ncomp,
                           const float2* __restrict__ Fc, float2* __restrict__ Ff, float scale) {
   const int hc = nc3 / 2 + 1, hf = nf3 / 2 + 1;
   const size_t ncc = size_t(nc1) * nc2 * hc, ncf = size_t(nf1) * nf2 * hf;
   const unsigned total = unsigned(ncf) * unsigned(ncomp);
   const unsigned stride = gridDim.x * blockDim.x;
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int c = int(e / unsigned(ncf));
-    const unsigned r = e - unsigned(c) * unsigned(ncf);
     int f1, f2, f3;
-    split3(r, unsigned(hf), unsigned(nf2), f1, f2, f3);
+    const int c = ix.split(e, f1, f2, f3);
     Ff[e] = prolong_elem(nf1, nf2, nc1, nc2, nc3, Fc + size_t(c) * ncc, f1, f2, f3, scale);
   }
 }
@@ -316,17 +317,15 @@ __device__ __forceinline__ float2 high_pass_elem(int n1, int n2, int n3,
   return make_float2(v.x * scale, v.y * scale);
 }
 
-__global__ void k_high_pass(int n1, int n2, int n3, int ncomp, const float2* __restrict__ Fin,
+__global__ void k_high_pass(Idx3 ix, int n1, int n2, int n3, int ncomp, const float2* __restrict__ Fin,
                             float2* __restrict__ Fout, float scale) {
   const int h = n3 / 2 + 1;
   const size_t nc = size_t(n1) * n2 * h;
   const unsigned total = unsigned(nc) * unsigned(ncomp);
   const unsigned stride = gridDim.x * blockDim.x;
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int c = int(e / unsigned(nc));
-    const unsigned r = e - unsigned(c) * unsigned(nc);
     int k1, k2, k3;
-    split3(r, unsigned(h), unsigned(n2), k1, k2, k3);
+    const int c = ix.split(e, k1, k2, k3);
     Fout[e] = high_pass_elem(n1, n2, n3, Fin + size_t(c) * nc, k1, k2, k3, scale);
   }
 }
@@ -334,25 +333,56 @@ __global__ void k_high_pass(int n1, int n2, int n3, int ncomp, const float2* __r
 // Fused end of the two-level apply: G = prolong(Fc) + high_pass(Ff) on the
 // fine half spectrum, flat over the elements (a CTA per n3/2 + 1 row left
 // most threads idle on the odd tail: 170 us -> memory speed at 256^3).
+// One warp per (component, k1, k2) row of the fine half spectrum: the row's
+// band test, coarse row and partial |k|^2 are computed once, lanes walk k3.
+// Rows and elements on the coarse Nyquist lines (alias-partner sums) take
+// the element functions; the arithmetic is the same everywhere.
 __global__ void k_prolong_plus_hp(int nf1, int nf2, int nf3, int nc1, int nc2, int nc3,
                                   const float2* __restrict__ Fc, const float2* __restrict__ Ff,
                                   float2* __restrict__ G, float scale_p, float scale_h,
                                   float beta, int order) {
   const int hf = nf3 / 2 + 1, hc = nc3 / 2 + 1;
   const size_t ncf = size_t(nf1) * nf2 * hf, ncc = size_t(nc1) * nc2 * hc;
-  const unsigned total = 3u * unsigned(ncf);
-  const unsigned stride = gridDim.x * blockDim.x;
-  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int c = int(e / unsigned(ncf));
-    const unsigned r = e - unsigned(c) * unsigned(ncf);
-    int k1, k2, k3;
-    split3(r, unsigned(hf), unsigned(nf2), k1, k2, k3);
-    const float2 a = prolong_elem(nf1, nf2, nc1, nc2, nc3, Fc + c * ncc, k1, k2, k3, scale_p);
-    // high pass of InvA F: the alias partners it pairs share |k|
+  const int b1 = nc1 / 2, b2 = nc2 / 2, b3 = nc3 / 2;  // coarse Nyquist = n / 4
+  const int lane = threadIdx.x & 31;
+  const int rows = 3 * nf1 * nf2;
+  const int wstride = gridDim.x * (blockDim.x >> 5);
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += wstride) {
+    const int c = row / (nf1 * nf2), k12 = row - c * nf1 * nf2;
+    const int k1 = k12 / nf2, k2 = k12 - k1 * nf2;
     const int nu1 = k1 <= nf1 / 2 ? k1 : k1 - nf1, nu2 = k2 <= nf2 / 2 ? k2 : k2 - nf2;
-    const float hs = scale_h * inv_symbol(nu1, nu2, k3, beta, order);
-    const float2 b = high_pass_elem(nf1, nf2, nf3, Ff + c * ncf, k1, k2, k3, hs);
-    G[e] = make_float2(a.x + b.x, a.y + b.y);
+    const int a1 = abs(nu1), a2 = abs(nu2);
+    const bool band = a1 <= b1 && a2 <= b2;
+    const bool nyq = a1 == b1 || a2 == b2;
+    const float s12 = float(nu1) * nu1 + float(nu2) * nu2;
+    const float2* F = Ff + size_t(c) * ncf;
+    const float2* Fr = F + size_t(k12) * hf;
+    float2* Gr = G + size_t(c) * ncf + size_t(k12) * hf;
+    const float2* Cr =
+        band ? Fc + size_t(c) * ncc + (size_t(nu1 < 0 ? nu1 + nc1 : nu1) * nc2 +
+                                       (nu2 < 0 ? nu2 + nc2 : nu2)) * hc
+             : nullptr;
+    for (int k3 = lane; k3 < hf; k3 += 32) {
+      float sym = s12 + float(k3) * k3;
+      if (order == 2) sym *= sym;
+      if (sym == 0.0f) sym = 1.0f;
+      const float hs = scale_h * __frcp_rn(beta * sym);
+      float2 out;
+      if (!band || k3 > b3) {  // outside the coarse band: high pass keeps InvA F
+        const float2 v = Fr[k3];
+        out = make_float2(0.0f + v.x * hs, 0.0f + v.y * hs);
+      } else if (!nyq && k3 != b3) {  // band interior: the prolongation alone
+        const float2 v = Cr[k3];
+        out = make_float2(v.x * scale_p + 0.0f, v.y * scale_p + 0.0f);
+      } else {  // coarse Nyquist lines: partner sums
+        const float2 a = prolong_elem(nf1, nf2, nc1, nc2, nc3, Fc + size_t(c) * ncc, k1, k2, k3,
+                                      scale_p);
+        const float2 b = high_pass_elem(nf1, nf2, nf3, F, k1, k2, k3, hs);
+        out = make_float2(a.x + b.x, a.y + b.y);
+      }
+      Gr[k3] = out;
+    }
   }
 }
 
@@ -382,7 +412,7 @@ SpecDesc spec_desc(vreg_ctx ctx, const Slab& s) {
   d.n2l = s.n2 / ctx->nranks;
   d.k2off = ctx->rank * d.n2l;
   d.nc = size_t(s.n1) * d.n2l * d.h;
-  require(3 * d.nc < (size_t(1) << 32), VREG_EDIM, "spectrum too large for 32-bit indexing");
+  require(3 * d.nc < (size_t(1) << 31), VREG_EDIM, "spectrum too large for 32-bit indexing");
   return d;
 }
 
@@ -421,7 +451,7 @@ void apply_symbol(vreg_ctx ctx, const SpecDesc& d, int ncomp, float2* F, double 
                   bool unit_zero, double scale) {
   Timed t(ctx, T_FFT, "spec_symbol");
   k_symbol<<<blocks_for(size_t(ncomp) * d.nc, 256), 256, 0, ctx->stream>>>(
-      d, ncomp, F, float(beta), inverse ? 1 : 0, unit_zero ? 1 : 0, float(scale), ctx->reg_order);
+      d, Idx3(unsigned(d.h), unsigned(d.n2l), d.nc), ncomp, F, float(beta), inverse ? 1 : 0, unit_zero ? 1 : 0, float(scale), ctx->reg_order);
   count_launch(ctx);
   check_launch();
 }
@@ -544,7 +574,7 @@ int vreg_restrict(vreg_ctx ctx, const vreg_grid* g, int ncomp, const float* f, f
     fft_forward(ctx, s, ncomp, f, Ff);
     // (Nc/Nf) partner sum, then the coarse inverse's 1/Nc: net 1/Nf
     k_restrict<<<blocks_for(dc.nc * ncomp, kT), kT, 0, ctx->stream>>>(
-        s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, ncomp, Ff, Fc, float(1.0 / double(s.global())));
+        Idx3(unsigned(dc.h), unsigned(sc.n2), dc.nc), s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, ncomp, Ff, Fc, float(1.0 / double(s.global())));
     count_launch(ctx);
     check_launch();
     fft_inverse(ctx, sc, ncomp, Fc, outc);
@@ -566,7 +596,7 @@ int vreg_prolong(vreg_ctx ctx, const vreg_grid* g, int ncomp, const float* fc, f
     fft_forward(ctx, sc, ncomp, fc, Fc);
     // (Nf/Nc)/nsplit, then the fine inverse's 1/Nf: net 1/(Nc nsplit)
     k_prolong<<<blocks_for(df.nc * ncomp, kT), kT, 0, ctx->stream>>>(
-        s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, ncomp, Fc, Ff, float(1.0 / double(sc.global())));
+        Idx3(unsigned(df.h), unsigned(s.n2), df.nc), s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, ncomp, Fc, Ff, float(1.0 / double(sc.global())));
     count_launch(ctx);
     check_launch();
     fft_inverse(ctx, s, ncomp, Ff, outf);
@@ -591,7 +621,7 @@ int vreg_high_pass(vreg_ctx ctx, const vreg_grid* g, int ncomp, const float* f, 
     float2* G = spec_buffer(ctx, d, ncomp, "spec_f2");
     fft_forward(ctx, s, ncomp, f, F);
     k_high_pass<<<blocks_for(d.nc * ncomp, kT), kT, 0, ctx->stream>>>(
-        s.n1, s.n2, s.n3, ncomp, F, G, float(1.0 / double(s.global())));
+        Idx3(unsigned(d.h), unsigned(s.n2), d.nc), s.n1, s.n2, s.n3, ncomp, F, G, float(1.0 / double(s.global())));
     count_launch(ctx);
     check_launch();
     fft_inverse(ctx, s, ncomp, G, out);
@@ -637,7 +667,7 @@ int vreg_two_level_begin(vreg_ctx ctx, const vreg_grid* g, const float* r3, doub
     fft_forward(ctx, s, 3, r3, F);
     const float rs = float(1.0 / double(s.global()));
     k_restrict_pair<<<blocks_for(dc.nc * 3, kT), kT, 0, ctx->stream>>>(
-        s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, F, Fc, Fs, rs, float(beta_pc), ctx->reg_order);
+        Idx3(unsigned(dc.h), unsigned(sc.n2), dc.nc), s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, F, Fc, Fs, rs, float(beta_pc), ctx->reg_order);
     count_launch(ctx);
     check_launch();
     fft_inverse(ctx, sc, 3, Fc, rc3);
@@ -657,7 +687,7 @@ int vreg_two_level_end(vreg_ctx ctx, const vreg_grid* g, const float* sc3, float
     float2* Fc = spec_buffer(ctx, dc, 3, "tl_Fc");
     float2* G = spec_buffer(ctx, df, 3, "tl_G");
     fft_forward(ctx, sc, 3, sc3, Fc);
-    k_prolong_plus_hp<<<blocks_for(df.nc * 3, kT), kT, 0, ctx->stream>>>(
+    k_prolong_plus_hp<<<blocks_for(size_t(3) * s.n1 * s.n2, kT / 32), kT, 0, ctx->stream>>>(
         s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, Fc, F, G, float(1.0 / double(sc.global())),
         float(1.0 / double(s.global())), float(ctx->tl_beta), ctx->reg_order);
     count_launch(ctx);

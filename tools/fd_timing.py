@@ -1,5 +1,7 @@
 """Device time of fd_grad / fd_div at 256^3 (kernel timers)."""
+import sys
 import torch
+sys.path.insert(0, ".")
 
 from paper_2008_12820_b200.engine import Context
 
