@@ -390,10 +390,25 @@ def run_ours(args):
             inner += st["inner"]
         barrier()
         pms = max_over_ranks(sorted(per)[napp // 2])
+        # where an apply's time goes (CUDA-event timers of the named scopes,
+        # rank 0; outside the timed applies above)
+        ctx.enable_timers(True)
+        ctx.kernel_stats(reset=True)
+        tb = ctx.timers()
+        for _ in range(3):
+            solver.precond("2linvh0", r, 0.5)
+        torch.cuda.synchronize()
+        ctx.enable_timers(False)
+        ks, ta = ctx.kernel_stats(), ctx.timers()
         extra["precond_2linvh0"] = {"ms_per_apply": pms, "applies_per_s": 1e3 / pms,
                                     "ms_each": [round(x, 3) for x in per],
                                     "timing": "median of 7 host wall-clock applies, device-synced",
-                                    "inner_cg_per_apply": inner / napp, "eps_k": 0.5}
+                                    "inner_cg_per_apply": inner / napp, "eps_k": 0.5,
+                                    "timers_ms_per_apply": {
+                                        k: round((ta[k] - tb[k]) / 3 * 1e3, 4)
+                                        for k in ta if ta[k] != tb[k]},
+                                    "scopes_ms_per_apply": {
+                                        k: round(v["seconds"] / 3 * 1e3, 4) for k, v in ks.items()}}
         # twice: the first run pays cuFFT plan creation for the coarse grid
         # and the pool's first allocations; the second is the steady state
         secs = []

@@ -135,6 +135,11 @@ const char* const kCatNames[T_COUNT] = {"fft",          "fd",           "sl",
 Timed::Timed(vreg_ctx ctx, int cat, const char* name) : ctx_(ctx), cat_(cat), name_(name) {
   nvtxRangePushA(name ? name : (cat >= 0 && cat < T_COUNT ? kCatNames[cat] : "vreg"));
   if (!ctx_->timers_on) return;
+  // scopes recorded into a CUDA graph (stream capture) are not timed: their
+  // events would never complete on their own
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(ctx_->stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+    return;
   if (ctx_->event_pool.empty()) {
     cudaEvent_t e;
     VB_CUDA(cudaEventCreate(&e));
@@ -148,6 +153,11 @@ Timed::Timed(vreg_ctx ctx, int cat, const char* name) : ctx_(ctx), cat_(cat), na
 Timed::~Timed() {
   nvtxRangePop();
   if (!a_) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(ctx_->stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    ctx_->event_pool.push_back(a_);  // began outside the capture: drop the sample
+    return;
+  }
   cudaEvent_t b;
   if (ctx_->event_pool.empty()) {
     if (cudaEventCreate(&b) != cudaSuccess) return;

@@ -327,6 +327,8 @@ class DevicePrecond {
       sc_.emplace(ce.make_vfield());
     }
     const vreg_grid g = eng_->vg();
+    std::optional<vb::Timed> phase;
+    phase.emplace(ctx, -1, "pc_2l_begin");
     if (eng_->workers() == 1) {
       check(vreg_two_level_begin(ctx, &g, r, beta_pc_, rc_->data(), sc_->data()));
     } else {
@@ -345,12 +347,14 @@ class DevicePrecond {
       check(vreg_inv_regop(ctx, &gc, rc_->data(), beta_pc_, sc_->data()));
       check(vreg_copy(ctx, &gc, 3, sc_->data(), sc0_->data()));
     }
+    phase.emplace(ctx, -1, "pc_2l_inner");
     if (split_h0())
       inner(ce, *gm_c_).solve_h0(gm_c_->data(), op_inv(ce), rc_->data(), sc_->data(), tol, cap_,
                                  acc_);
     else
       inner(ce, *gm_c_).solve(op_h0(ce, *gm_c_), op_inv(ce), rc_->data(), sc_->data(), tol,
                               cap_, true, acc_);
+    phase.emplace(ctx, -1, "pc_2l_end");
     if (eng_->workers() == 1) {
       check(vreg_two_level_end(ctx, &g, sc_->data(), z));
     } else {

@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_gather_tile(
 // turn: D_c = -(dt/2)/h_c (v_c + I[v_c](mid)). Tiles whose box exceeds the
 // budget take the per-point global path.
 template <int DEG, bool DIST>
-__global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS) k_chars_tile(
+__global__ void __launch_bounds__(TILE_THREADS, DIST ? 2 : TILE_MIN_BLOCKS) k_chars_tile(
     Geo g, SrcField<DIST> s1, SrcField<DIST> s2, SrcField<DIST> s3, const float* __restrict__ v,
     float m1, float m2, float m3, float c1, float c2, float c3, int box_cap_words,
     float* __restrict__ D) {
