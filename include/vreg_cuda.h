@@ -85,7 +85,7 @@ int vreg_ctx_set_deterministic(vreg_ctx ctx, int on);
  * seminorm / h0_matvec / the GN matvec: 1 = H1, symbol |k|^2 (the
  * reference, spectral.cpp:61-63; default), 2 = H2, symbol |k|^4 (B200
  * extension named by the north star; no reference oracle -- analytic
- * single-mode checks in tests/test_gpu_kernels.py). */
+ * single-mode checks in tests/test_gpu_h2.py). */
 int vreg_ctx_set_reg_order(vreg_ctx ctx, int order);
 /* The stream all calls on ctx are ordered on (cudaStream_t). */
 int vreg_ctx_get_stream(vreg_ctx ctx, void** stream);
@@ -207,7 +207,8 @@ int vreg_high_pass(vreg_ctx, const vreg_grid*, int ncomp, const float* f, float*
  * on one rank: begin writes rc3 = restrict(r3) and sc3 = restrict(InvA r3) on
  * the coarse grid (n/2) from ONE forward transform of r3 and keeps InvA r3's
  * spectrum; end writes out3 = prolong(sc3) + high_pass(InvA r3) with one
- * inverse transform. VREG_ECONFIG on several ranks. */
+ * inverse transform. rc3 may be NULL (the split H0 solve starts from sc3
+ * alone). VREG_ECONFIG on several ranks. */
 int vreg_two_level_begin(vreg_ctx ctx, const vreg_grid* g, const float* r3, double beta_pc,
                          float* rc3, float* sc3);
 int vreg_two_level_end(vreg_ctx ctx, const vreg_grid* g, const float* sc3, float* out3);

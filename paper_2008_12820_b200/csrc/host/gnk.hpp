@@ -330,7 +330,9 @@ class DevicePrecond {
     std::optional<vb::Timed> phase;
     phase.emplace(ctx, -1, "pc_2l_begin");
     if (eng_->workers() == 1) {
-      check(vreg_two_level_begin(ctx, &g, r, beta_pc_, rc_->data(), sc_->data()));
+      // the split inner solve starts from s_c0 alone (r0 = -G s_c0)
+      check(vreg_two_level_begin(ctx, &g, r, beta_pc_, split_h0() ? nullptr : rc_->data(),
+                                 sc_->data()));
     } else {
       // slab-distributed: restrict(InvA_f r) = InvA_c restrict(r) mode by
       // mode, so high_pass(InvA_f r) = InvA_f r - prolong(s_c0) with the

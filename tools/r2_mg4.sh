@@ -9,7 +9,7 @@ for size in 256 512; do
     bench.py --gpus $N --steps 10 --warmup 3 --size $size --no-cpu > gpurun_out/scale_g${N}_s${size}.json 2> gpurun_out/scale_g${N}_s${size}.err
   echo "bench g$N s$size rc=$?"
 done; done
-timeout 600 python bench.py --gpus 1 --steps 10 --warmup 3 --size 512 --no-cpu > gpurun_out/scale_g1_s512.json 2> gpurun_out/scale_g1_s512.err
+for size in 256 512; do timeout 600 python bench.py --gpus 1 --steps 10 --warmup 3 --size $size --no-cpu > gpurun_out/scale_g1_s$size.json 2> gpurun_out/scale_g1_s$size.err; done
 echo "bench g1 s512 rc=$?"
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29561 tools/mgpu_check.py 512 > gpurun_out/mgpu512_p4.log 2>&1
 echo "mgpu512 p4 rc=$?"
