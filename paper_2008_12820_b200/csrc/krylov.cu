@@ -11,8 +11,6 @@
 
 namespace vb {
 
-int chunks_per_plane(const Slab& s);
-
 namespace {
 
 constexpr int KT = 256;  // threads of the partial-sum kernels
@@ -416,7 +414,9 @@ inline void cuda_ok(cudaError_t e, const char* what) {
 }  // namespace
 
 Krylov::Krylov(vreg_ctx ctx, const Slab& s, bool fp64) : ctx_(ctx), s_(s), fp64_(fp64) {
-  chunks_ = chunks_per_plane(s);
+  // 2048-element chunks (8 per thread): enough CTAs that the streaming
+  // update kernels keep their loads in flight (8192 left them latency-bound)
+  chunks_ = int((s.plane() + 2047) / 2048);
   n3_ = 3 * s.local();
   require(s.n1 <= 1024, VREG_ECONFIG, "Krylov fold supports n1 <= 1024");
   const size_t es = fp64 ? sizeof(double) : sizeof(float);

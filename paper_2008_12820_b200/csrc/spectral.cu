@@ -381,7 +381,7 @@ __global__ void k_prolong_plus_hp(int nf1, int nf2, int nf3, int nc1, int nc2, i
         float sym = s12 + float(k3) * k3;
         if (order == 2) sym *= sym;
         if (sym == 0.0f) sym = 1.0f;
-        const float hs = scale_h * __frcp_rn(beta * sym);
+        const float hs = __fdividef(scale_h, beta * sym);  // approximate reciprocal (2 ulp)
         float2 out;
         if (!band || k3 > b3) {  // outside the coarse band: high pass keeps InvA F
           out = make_float2(0.0f + v[u].x * hs, 0.0f + v[u].y * hs);
