@@ -45,37 +45,43 @@ struct SideRoute {
 };
 }  // namespace
 
-// The regulariser branch (R2C -> symbol -> C2R, plus the slab all-to-alls
-// on several GPUs) is independent of the transport sweeps until the final
-// assembly, so it runs on a side stream (own NCCL communicator) and
-// overlaps the latency-bound SL kernels.
+// The regulariser branch (separable passes, plus the slab transposes on
+// several GPUs) is independent of the transport sweeps until the final
+// assembly, so it runs on a side stream (own NCCL communicator) beside them.
 void gn_matvec(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int degree,
                const float* grads, double beta, const float* vt3, float* out3) {
   const size_t N = s.local();
   float* psi = sl_matvec_psi(ctx, s, disp3, flags, degree);
   float* reg = static_cast<float*>(workspace(ctx, "mv_reg", 3 * N * sizeof(float)));
-  static const bool serial = [] {  // diagnostics: VREG_SERIAL_MATVEC=1 -> no overlap
+  // Where the regulariser branch runs: 0 serial on the main stream, 1 on the
+  // side stream beside the inc-state steps, 2 beside the transpose sweeps.
+  // The persistent step sweeps hold every SM, so a branch beside them only
+  // delays their CTAs (steps 296 vs 197 us at 256^3); beside the transpose
+  // sweeps (many short CTAs) it overlaps: 2.715 (2) vs 2.764 (1) vs 2.789 ms
+  // (0) on one GPU. On several GPUs the sweeps carry the boundary bands and
+  // reverse exchanges, and mode 1 measured faster at 256^3 per GPU
+  // (3.40 vs 3.65 ms). VREG_MATVEC_OVERLAP overrides, VREG_SERIAL_MATVEC=1
+  // forces 0.
+  static const int env_mode = [] {
     const char* e = std::getenv("VREG_SERIAL_MATVEC");
-    return e && e[0] == '1';
+    if (e && e[0] == '1') return 0;
+    const char* o = std::getenv("VREG_MATVEC_OVERLAP");
+    return o ? std::atoi(o) : -1;
   }();
-  if (serial) {
-    spectral_regop(ctx, s, vt3, beta, false, false, reg);
-    sl_inc_state(ctx, s, disp3, flags, degree, grads, vt3, nullptr, psi + size_t(s.nt) * N);
-    sl_transpose_sweeps(ctx, s, disp3, flags, degree, psi);
-    sl_assemble(ctx, s, 1, psi, grads, reg, out3);
-    return;
-  }
-  // (overlapping the transpose sweeps instead measured slower)
-  VB_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
-  VB_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-  {
+  const int mode = env_mode >= 0 ? env_mode : (ctx->nranks > 1 ? 1 : 2);
+  auto side_regop = [&] {
+    VB_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
+    VB_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     SideRoute route(ctx);
     spectral_regop(ctx, s, vt3, beta, false, false, reg);
     VB_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
-  }
+  };
+  if (mode == 0) spectral_regop(ctx, s, vt3, beta, false, false, reg);
+  if (mode == 1) side_regop();
   sl_inc_state(ctx, s, disp3, flags, degree, grads, vt3, nullptr, psi + size_t(s.nt) * N);
+  if (mode == 2) side_regop();
   sl_transpose_sweeps(ctx, s, disp3, flags, degree, psi);
-  VB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+  if (mode != 0) VB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
   sl_assemble(ctx, s, 1, psi, grads, reg, out3);
 }
 
