@@ -1,0 +1,73 @@
+"""The measurement switches keep the path's results: each
+alternative -- two-operator H0 inner solves, the regulariser serial or
+beside the inc-state steps, eager Krylov loops, the cp.async tile kernels
+instead of the TMA pipeline -- runs in its own process (the library reads
+the switches once) and is checked against the unmodified reference at 64^3:
+GN matvec (rel L2 <= 1e-5), InvA (1e-5) and 2LInvH0 (1e-4, equal inner
+iterations; precond.hpp:133-162), and a 2 GN x 3 PCG 2LInvH0 solve
+(mismatch within 1e-3 of the reference's)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import json, sys
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+from oracle import ref
+from paper_2008_12820_b200 import Context
+from paper_2008_12820_b200.solver import Config, Solver
+
+n, beta = 64, 1e-3
+dev = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float32, device="cuda")
+rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+m0, v, m1 = ref.syn(n)
+ctx = Context(0)
+s = Solver(ctx, n, Config(continuation=False, beta_target=beta))
+s.syn_images()
+s.linearize(dev(0.5 * v), beta)
+r = ref.Session(m0, m1, 0.5 * v, beta, ref.Config(continuation=False, beta_target=beta))
+g = r.gradient()
+out = {"matvec": rel(s.matvec(dev(-g)).double().cpu().numpy(), r.matvec(-g))}
+for kind in ("inva", "2linvh0"):
+    z, st = s.precond(kind, dev(-g), 0.5)
+    zr, rst = r.precond(kind, -g, 0.5)
+    out[kind] = rel(z.double().cpu().numpy(), zr)
+    out[kind + "_inner"] = [int(st["inner"]), int(rst["inner"])]
+cfg = Config(continuation=False, beta_target=beta, fixed_gn=2, fixed_pcg=3, precond="2linvh0")
+s2 = Solver(ctx, n, cfg)
+s2.syn_images()
+_, rep, _ = s2.register()
+_, rrep, _ = ref.register(m0, m1, ref.Config(continuation=False, beta_target=beta, fixed_gn=2,
+                                             fixed_pcg=3, precond="2linvh0"))
+out["solve"] = abs(rep["final_mismatch"] / rrep["final_mismatch"] - 1)
+print("RESULT " + json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env", [
+    {"VREG_H0_SPLIT": "0"},
+    {"VREG_MATVEC_OVERLAP": "0"},
+    {"VREG_MATVEC_OVERLAP": "1"},
+    {"VREG_PCG_GRAPH": "0"},
+    {"VREG_SL_PIPE": "0"},
+], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_switch_keeps_parity(env):
+    p = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = [ln for ln in p.stdout.splitlines() if ln.startswith("RESULT ")][-1]
+    res = json.loads(line[len("RESULT "):])
+    assert res["matvec"] < 1e-5, res
+    assert res["inva"] < 1e-5, res
+    assert res["2linvh0"] < 1e-4, res
+    assert res["2linvh0_inner"][0] == res["2linvh0_inner"][1], res
+    assert res["solve"] < 1e-3, res
