@@ -471,6 +471,7 @@ void apply_symbol(vreg_ctx ctx, const SpecDesc& d, int ncomp, float2* F, double 
 
 bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, float* out3,
                      bool unit_zero);
+bool inva_fused(vreg_ctx ctx, const Slab& s, const float* v3, double beta, float* out3);
 
 // out3 = beta A v3 (or its inverse); used by the fused matvec too. The
 // forward operator is separable (|k|^2 = k1^2 + k2^2 + k3^2; a unit null-mode
@@ -484,6 +485,7 @@ void spectral_regop(vreg_ctx ctx, const Slab& s, const float* v3, double beta, b
   // first by the second's |k|^2 (measured ~1e-5 relative on single modes)
   if (!inverse && ctx->reg_order == 1 && regop_separable(ctx, s, v3, beta, out3, unit_zero))
     return;
+  if (inverse && inva_fused(ctx, s, v3, beta, out3)) return;
   const SpecDesc d = spec_desc(ctx, s);
   float2* F = spec_buffer(ctx, d, 3, "spec3");
   fft_forward(ctx, s, 3, v3, F);
