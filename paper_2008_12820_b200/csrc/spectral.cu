@@ -703,6 +703,9 @@ int vreg_two_level_end(vreg_ctx ctx, const vreg_grid* g, const float* sc3, float
     float2* Fc = spec_buffer(ctx, dc, 3, "tl_Fc");
     float2* G = spec_buffer(ctx, df, 3, "tl_G");
     fft_forward(ctx, sc, 3, sc3, Fc);
+    // (fusing this pass with the x1 pass of the inverse -- plane C2R after
+    // one pencil kernel, like InvA -- measured slower: 1.94 vs 1.88 ms per
+    // apply, the pencil kernel's strided k1 reads at 224 us)
     k_prolong_plus_hp<<<blocks_for(size_t(3) * s.n1 * s.n2, kT / 32), kT, 0, ctx->stream>>>(
         s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, Fc, F, G, float(1.0 / double(sc.global())),
         float(1.0 / double(s.global())), float(ctx->tl_beta), ctx->reg_order);
