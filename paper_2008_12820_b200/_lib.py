@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libvreg_b200.so")
+# VREG_LIB_PATH: an alternative in-tree build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("VREG_LIB_PATH") or os.path.join(PKG, "libvreg_b200.so")
 
 
 class VregGrid(C.Structure):

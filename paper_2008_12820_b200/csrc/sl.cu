@@ -393,7 +393,9 @@ __global__ void __launch_bounds__(TILE_THREADS, DIST ? 2 : TILE_MIN_BLOCKS) k_ch
 // order, so the last bits can differ between runs (VREG_DETERMINISTIC=1 /
 // vreg_ctx_set_deterministic selects the fixed-point variant below).
 // (two CTAs per SM at 96 registers, leaving room for the regulariser's CTAs
-// beside it, measured 299 vs 265 us per sweep: three CTAs per SM stay)
+// beside it, measured 299 vs 265 us per sweep: three CTAs per SM stay; the
+// multi-rank variant runs spill-free at two, within 1% of three CTAs at 80
+// registers with spills around the fallback calls, p = 2)
 template <int DEG, bool DIST>
 __global__ void __launch_bounds__(TILE_THREADS, DIST ? 2 : TILE_MIN_BLOCKS) k_scatter_tile_fp(Geo g, DstField<DIST> dst,
                                                                   const int* __restrict__ boxes,
