@@ -79,14 +79,12 @@ double* pinned(vreg_ctx ctx, size_t n) {
   return ctx->h_pinned;
 }
 
-namespace {
-// Cached R2C / C2R plan pair under `key`, made by `make(r2c, c2r, &w1, &w2)`;
-// all plans share one work area, and follow the context's current stream
-// (side-stream branches, graph-capture streams of the Krylov solver).
-template <class Make>
-FftPlans& cached_plans(vreg_ctx ctx, const std::tuple<int, int, int, int>& key, Make make) {
+FftPlans& fft_plans(vreg_ctx ctx, int n1, int n2, int n3, int batch) {
+  auto key = std::make_tuple(n1, n2, n3, batch);
   auto it = ctx->plans.find(key);
   if (it != ctx->plans.end()) {
+    // plans follow the context's current stream (side-stream branches,
+    // graph-capture streams of the Krylov solver)
     if (it->second.stream != ctx->stream) {
       VB_CUFFT(cufftSetStream(it->second.r2c, ctx->stream));
       VB_CUFFT(cufftSetStream(it->second.c2r, ctx->stream));
@@ -96,12 +94,18 @@ FftPlans& cached_plans(vreg_ctx ctx, const std::tuple<int, int, int, int>& key, 
   }
   std::lock_guard<std::mutex> lock(g_plan_mutex);
   FftPlans p;
+  int n[3] = {n1, n2, n3};
+  const long long N = (long long)n1 * n2 * n3;
+  const long long NC = (long long)n1 * n2 * (n3 / 2 + 1);
   size_t w1 = 0, w2 = 0;
   VB_CUFFT(cufftCreate(&p.r2c));
   VB_CUFFT(cufftCreate(&p.c2r));
   VB_CUFFT(cufftSetAutoAllocation(p.r2c, 0));
   VB_CUFFT(cufftSetAutoAllocation(p.c2r, 0));
-  make(p.r2c, p.c2r, &w1, &w2);
+  VB_CUFFT(cufftMakePlanMany(p.r2c, 3, n, nullptr, 1, int(N), nullptr, 1, int(NC),
+                             CUFFT_R2C, batch, &w1));
+  VB_CUFFT(cufftMakePlanMany(p.c2r, 3, n, nullptr, 1, int(NC), nullptr, 1, int(N),
+                             CUFFT_C2R, batch, &w2));
   p.work = w1 > w2 ? w1 : w2;
   if (p.work > ctx->fft_work_size) {
     if (ctx->fft_work) VB_CUDA(cudaFreeAsync(ctx->fft_work, ctx->stream));
@@ -118,35 +122,6 @@ FftPlans& cached_plans(vreg_ctx ctx, const std::tuple<int, int, int, int>& key, 
   VB_CUFFT(cufftSetStream(p.c2r, ctx->stream));
   p.stream = ctx->stream;
   return ctx->plans.emplace(key, p).first->second;
-}
-}  // namespace
-
-FftPlans& fft_plans(vreg_ctx ctx, int n1, int n2, int n3, int batch) {
-  return cached_plans(ctx, std::make_tuple(n1, n2, n3, batch),
-                      [&](cufftHandle r2c, cufftHandle c2r, size_t* w1, size_t* w2) {
-                        int n[3] = {n1, n2, n3};
-                        const long long N = (long long)n1 * n2 * n3;
-                        const long long NC = (long long)n1 * n2 * (n3 / 2 + 1);
-                        VB_CUFFT(cufftMakePlanMany(r2c, 3, n, nullptr, 1, int(N), nullptr, 1,
-                                                   int(NC), CUFFT_R2C, batch, w1));
-                        VB_CUFFT(cufftMakePlanMany(c2r, 3, n, nullptr, 1, int(NC), nullptr, 1,
-                                                   int(N), CUFFT_C2R, batch, w2));
-                      });
-}
-
-// 2-D transforms of `batch` (x2, x3) planes, complex rows padded to hp
-// (spec_axis.cu inva_fused); keyed apart from the 3-D plans by -hp.
-FftPlans& plane_plans(vreg_ctx ctx, int n1, int n2, int n3, int hp, int batch) {
-  (void)n1;
-  return cached_plans(ctx, std::make_tuple(-hp, n2, n3, batch),
-                      [&](cufftHandle r2c, cufftHandle c2r, size_t* w1, size_t* w2) {
-                        int n[2] = {n2, n3};
-                        int re[2] = {n2, n3}, ce[2] = {n2, hp};
-                        VB_CUFFT(cufftMakePlanMany(r2c, 2, n, re, 1, n2 * n3, ce, 1, n2 * hp,
-                                                   CUFFT_R2C, batch, w1));
-                        VB_CUFFT(cufftMakePlanMany(c2r, 2, n, ce, 1, n2 * hp, re, 1, n2 * n3,
-                                                   CUFFT_C2R, batch, w2));
-                      });
 }
 
 namespace {

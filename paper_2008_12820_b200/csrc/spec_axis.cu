@@ -226,79 +226,6 @@ __global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 2) k_axis_d2(int n1
   }
 }
 
-// InvA (and the H2 inverse) on one GPU as plane transforms around one fused
-// x1 pass: a 2-D R2C over every (x2, x3) plane leaves x1 in real space; this
-// kernel runs, per complex pencil (component, k2, k3) along x1, the same
-// four-step FFT as k_axis_d2, multiplies by coef / (beta |k|^order) (zero
-// mode 1 / beta, spectral.cpp:72-93) and transforms back; a 2-D C2R per plane
-// finishes. Three passes over the spectrum instead of the 3-D route's six
-// plus the symbol pass. Rows of the plane spectra are padded to hp (a
-// multiple of NP) so a tile of NP consecutive k3 pencils never straddles a
-// row; the padding is transformed and ignored.
-template <int N>
-__global__ void __launch_bounds__(AX_THREADS, N <= 256 ? 3 : 2) k_inva_x1(
-    int n2, int hp, int h, int tiles, float2* __restrict__ F, const float2* __restrict__ tw,
-    float coef, float beta, int order) {
-  constexpr int T1 = AxisShape<N>::T1, NP = AxisShape<N>::NP;
-  constexpr int R2 = N / T1;
-  constexpr int SK = T1 + 1, SP = R2 * SK + 1;
-  extern __shared__ float2 S[];
-  const int nb = hp / NP;
-  const size_t js = size_t(n2) * hp;  // x1 stride of the plane spectra
-  for (int t = blockIdx.x; t < 3 * tiles; t += gridDim.x) {
-    const int comp = t / tiles, tile = t - comp * tiles;
-    const int k2 = tile / nb, kb = tile - k2 * nb;
-    const int n1 = int(threadIdx.x) / NP, p = int(threadIdx.x) % NP;
-    const int k3 = kb * NP + p;
-    const size_t off = (size_t(comp) * N * n2 + k2) * hp + k3 + size_t(n1) * js;
-    const float f2 = float(k2 <= n2 / 2 ? k2 : k2 - n2);
-    const float s23 = f2 * f2 + float(k3) * float(k3);
-    float2 a[R2];
-#pragma unroll
-    for (int m = 0; m < R2; ++m) a[m] = F[off + size_t(T1 * m) * js];
-    dft<R2, -1>(a);
-    float2* Sp = S + p * SP;
-#pragma unroll
-    for (int q = 0; q < R2; ++q) {
-      if (q != 0 && n1 != 0) a[q] = cmul(a[q], __ldg(tw + n1 * q));
-      Sp[q * SK + n1] = a[q];
-    }
-    __syncthreads();
-    for (int q = n1; q < R2; q += T1) {
-      float2 b[T1];
-#pragma unroll
-      for (int j = 0; j < T1; ++j) b[j] = Sp[q * SK + j];
-      dft<T1, -1>(b);
-#pragma unroll
-      for (int k1 = 0; k1 < T1; ++k1) {
-        const int f = q + R2 * k1;
-        const float f1 = float(f <= N / 2 ? f : f - N);
-        float sym = f1 * f1 + s23;
-        if (order == 2) sym *= sym;
-        if (sym == 0.0f) sym = 1.0f;
-        const float m = coef / (beta * sym);
-        b[k1].x *= m;
-        b[k1].y *= m;
-      }
-      dft<T1, 1>(b);
-#pragma unroll
-      for (int j = 0; j < T1; ++j) Sp[q * SK + j] = b[j];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < R2; ++q) {
-      a[q] = Sp[q * SK + n1];
-      if (q != 0 && n1 != 0) a[q] = cmul_conj(a[q], __ldg(tw + n1 * q));
-    }
-    dft<R2, 1>(a);
-    if (k3 < h) {
-#pragma unroll
-      for (int m = 0; m < R2; ++m) F[off + size_t(T1 * m) * js] = a[m];
-    }
-    __syncthreads();  // S is reused by the next tile
-  }
-}
-
 bool axis_size_ok(int n) { return n >= 32 && n <= 1024 && (n & (n - 1)) == 0; }
 
 const float2* twiddles(vreg_ctx ctx, int n) {
@@ -597,67 +524,6 @@ bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, 
     launch_axis<1>(ctx, loc, s.n1, v3, out3, beta, 1, cap);
   else
     dist_axis1(ctx, s, v3, out3, beta, cap);
-  return true;
-}
-
-
-// Plane (2-D, per x1 plane) R2C / C2R plans over ncomp * n1 planes, with the
-// complex rows padded to hp elements.
-FftPlans& plane_plans(vreg_ctx ctx, int n1, int n2, int n3, int hp, int batch);
-
-// out3 = InvA v3 (regop inverse, spectral.cpp:72-93) through plane transforms
-// and k_inva_x1; false outside the fast path (one GPU, x1 a power of two in
-// [32, 1024], even x3) or with VREG_INVA_3D=1.
-bool inva_fused(vreg_ctx ctx, const Slab& s, const float* v3, double beta, float* out3) {
-  static const bool off = [] {
-    const char* e = std::getenv("VREG_INVA_3D");
-    return e && e[0] == '1';
-  }();
-  if (off || ctx->nranks > 1 || !axis_size_ok(s.n1) || (s.n3 & 1)) return false;
-  const int h = s.n3 / 2 + 1;
-  const int np = s.n1 <= 512 ? AX_THREADS / 16 : AX_THREADS / 32;
-  const int hp = (h + np - 1) / np * np;
-  const size_t elems = size_t(3) * s.n1 * s.n2 * hp;
-  if (2 * elems >= (size_t(1) << 31)) return false;
-  float2* F = static_cast<float2*>(workspace(ctx, "inva_planes", elems * sizeof(float2)));
-  FftPlans& pl = plane_plans(ctx, s.n1, s.n2, s.n3, hp, 3 * s.n1);
-  {
-    Timed t(ctx, T_FFT, "fft_r2c_planes");
-    VB_CUFFT(cufftExecR2C(pl.r2c, const_cast<float*>(v3), reinterpret_cast<cufftComplex*>(F)));
-  }
-  {
-    Timed t(ctx, T_FFT, "spec_inva_x1");
-    const float2* tw = twiddles(ctx, s.n1);
-    const int tiles = s.n2 * (hp / np);
-    const float coef = float(1.0 / double(s.global()));
-    const int order = ctx->reg_order;
-#define VB_INVA_CASE(NN)                                                                    \
-  case NN: {                                                                                \
-    const size_t smem = size_t(AxisShape<NN>::NP) *                                         \
-                        ((NN / AxisShape<NN>::T1) * (AxisShape<NN>::T1 + 1) + 1) * sizeof(float2); \
-    smem_optin(reinterpret_cast<const void*>(k_inva_x1<NN>), int(smem));                    \
-    k_inva_x1<NN><<<3 * tiles, AX_THREADS, smem, ctx->stream>>>(s.n2, hp, h, tiles, F, tw,  \
-                                                                coef, float(beta), order);  \
-    break;                                                                                  \
-  }
-    switch (s.n1) {
-      VB_INVA_CASE(32)
-      VB_INVA_CASE(64)
-      VB_INVA_CASE(128)
-      VB_INVA_CASE(256)
-      VB_INVA_CASE(512)
-      VB_INVA_CASE(1024)
-      default:
-        return false;
-    }
-#undef VB_INVA_CASE
-    count_launch(ctx);
-    check_launch();
-  }
-  {
-    Timed t(ctx, T_FFT, "fft_c2r_planes");
-    VB_CUFFT(cufftExecC2R(pl.c2r, reinterpret_cast<cufftComplex*>(F), out3));
-  }
   return true;
 }
 

@@ -471,7 +471,6 @@ void apply_symbol(vreg_ctx ctx, const SpecDesc& d, int ncomp, float2* F, double 
 
 bool regop_separable(vreg_ctx ctx, const Slab& s, const float* v3, double beta, float* out3,
                      bool unit_zero);
-bool inva_fused(vreg_ctx ctx, const Slab& s, const float* v3, double beta, float* out3);
 
 // out3 = beta A v3 (or its inverse); used by the fused matvec too. The
 // forward operator is separable (|k|^2 = k1^2 + k2^2 + k3^2; a unit null-mode
@@ -485,7 +484,9 @@ void spectral_regop(vreg_ctx ctx, const Slab& s, const float* v3, double beta, b
   // first by the second's |k|^2 (measured ~1e-5 relative on single modes)
   if (!inverse && ctx->reg_order == 1 && regop_separable(ctx, s, v3, beta, out3, unit_zero))
     return;
-  if (inverse && inva_fused(ctx, s, v3, beta, out3)) return;
+  // (InvA as 2-D plane transforms around one fused x1 FFT/symbol/IFFT pencil
+  // pass: 86 vs 91 us per 128^3 apply, but its 226 MB plane workspace at
+  // 256^3 slowed the registration's gradient phase by 10 ms; not kept)
   const SpecDesc d = spec_desc(ctx, s);
   float2* F = spec_buffer(ctx, d, 3, "spec3");
   fft_forward(ctx, s, 3, v3, F);
@@ -704,8 +705,8 @@ int vreg_two_level_end(vreg_ctx ctx, const vreg_grid* g, const float* sc3, float
     float2* G = spec_buffer(ctx, df, 3, "tl_G");
     fft_forward(ctx, sc, 3, sc3, Fc);
     // (fusing this pass with the x1 pass of the inverse -- plane C2R after
-    // one pencil kernel, like InvA -- measured slower: 1.94 vs 1.88 ms per
-    // apply, the pencil kernel's strided k1 reads at 224 us)
+    // one pencil kernel -- measured slower: 1.94 vs 1.88 ms per apply, the
+    // pencil kernel's strided k1 reads at 224 us)
     k_prolong_plus_hp<<<blocks_for(size_t(3) * s.n1 * s.n2, kT / 32), kT, 0, ctx->stream>>>(
         s.n1, s.n2, s.n3, sc.n1, sc.n2, sc.n3, Fc, F, G, float(1.0 / double(sc.global())),
         float(1.0 / double(s.global())), float(ctx->tl_beta), ctx->reg_order);

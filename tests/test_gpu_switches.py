@@ -2,8 +2,7 @@
 alternative -- two-operator H0 inner solves, the regulariser serial or
 beside the inc-state steps, eager Krylov loops, the cp.async tile kernels
 instead of the TMA pipeline -- runs in its own process (the library reads
-the switches once), as do the 3-D cuFFT route for InvA, and is checked
-against the unmodified reference at 64^3:
+the switches once) and is checked against the unmodified reference at 64^3:
 GN matvec (rel L2 <= 1e-5), InvA (1e-5) and 2LInvH0 (1e-4, equal inner
 iterations; precond.hpp:133-162), and a 2 GN x 3 PCG 2LInvH0 solve
 (mismatch within 1e-3 of the reference's)."""
@@ -60,7 +59,6 @@ print("RESULT " + json.dumps(out))
     {"VREG_MATVEC_OVERLAP": "1"},
     {"VREG_PCG_GRAPH": "0"},
     {"VREG_SL_PIPE": "0"},
-    {"VREG_INVA_3D": "1"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_switch_keeps_parity(env):
     p = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, env={**os.environ, **env},
