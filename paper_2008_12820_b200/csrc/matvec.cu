@@ -59,16 +59,18 @@ void gn_matvec(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int d
   // delays their CTAs (steps 296 vs 197 us at 256^3); beside the transpose
   // sweeps (many short CTAs) it overlaps: 2.715 (2) vs 2.764 (1) vs 2.789 ms
   // (0) on one GPU. On several GPUs the sweeps carry the boundary bands and
-  // reverse exchanges, and mode 1 measured faster at 256^3 per GPU
-  // (3.40 vs 3.65 ms). VREG_MATVEC_OVERLAP overrides, VREG_SERIAL_MATVEC=1
-  // forces 0.
+  // reverse exchanges: mode 1 is faster at 256^3 per GPU (3.40 vs 3.65 ms,
+  // p = 2), mode 2 from 512^3 per GPU on (25.32 vs 25.67 ms at p = 2, 26.24
+  // vs 26.42 ms at p = 4). VREG_MATVEC_OVERLAP overrides,
+  // VREG_SERIAL_MATVEC=1 forces 0.
   static const int env_mode = [] {
     const char* e = std::getenv("VREG_SERIAL_MATVEC");
     if (e && e[0] == '1') return 0;
     const char* o = std::getenv("VREG_MATVEC_OVERLAP");
     return o ? std::atoi(o) : -1;
   }();
-  const int mode = env_mode >= 0 ? env_mode : (ctx->nranks > 1 ? 1 : 2);
+  const int mode =
+      env_mode >= 0 ? env_mode : (ctx->nranks > 1 && N < (size_t(1) << 26) ? 1 : 2);
   auto side_regop = [&] {
     VB_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
     VB_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
