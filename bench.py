@@ -460,13 +460,25 @@ def run_ours(args):
         # dominant kernel by device time inside the timed region
         dom = max(kstats.items(), key=lambda kv: kv[1]["seconds"]) if kstats else None
         roof = None
+        BPV = {"sl_scatter_sweep": 28.0, "sl_inc_step": 24.0, "sl_assemble": 16.0 * (NT + 1) + 24.0,
+               "sl_inc_init": 12.0 * (NT + 1) + 16 + 4.0 * NT, "spec_axis3": 24.0,
+               "spec_axis2": 36.0, "spec_axis1": 36.0}
+        # every timed kernel group of the matvec against the same peak (the
+        # dominant one below is the headline `roofline`)
+        by_kernel = {}
+        for kname, kst in kstats.items():
+            if kname in BPV and kst["count"]:
+                per = kst["seconds"] / kst["count"]
+                ach = BPV[kname] * (Nvox // world) / per / 1e9
+                by_kernel[kname] = {"launch_us": round(per * 1e6, 1), "launches": kst["count"],
+                                    "bytes_per_voxel": BPV[kname], "achieved_gbs": round(ach, 1),
+                                    "frac": round(ach / peak, 3)}
+        extra["roofline_by_kernel"] = by_kernel
         if dom:
             name, st = dom
             per_launch_s = st["seconds"] / max(st["count"], 1)
             Nloc = Nvox // world
-            bpv = {"sl_scatter_sweep": 28.0, "sl_inc_step": 24.0, "sl_assemble": 16.0 * (NT + 1) + 24.0,
-                   "sl_inc_init": 12.0 * (NT + 1) + 16 + 4.0 * NT, "spec_axis3": 24.0,
-                   "spec_axis2": 36.0, "spec_axis1": 36.0}.get(name)
+            bpv = BPV.get(name)
             traffic = ncu_traffic()
             roof = {"bound": "hbm", "kernel": name, "peak": peak, "peak_kind": peak_kind,
                     "unit": "GB/s", "bytes_per_voxel": bpv,
