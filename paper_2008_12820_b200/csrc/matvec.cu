@@ -19,9 +19,10 @@ namespace vb {
 
 struct SpecDesc;
 void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int degree,
-                  const float* grads, const float* vt3, float* mt_all, float* psi_out);
+                  const float* grads, const float* vt3, float* mt_all, float* psi_out,
+                  float* zero_slices);
 void sl_transpose_sweeps(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int degree,
-                         float* psi);
+                         float* psi, bool prezeroed);
 float* sl_matvec_psi(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int degree);
 void sl_assemble(vreg_ctx ctx, const Slab& s, int descending, const float* sl, const float* grads,
                  const float* reg, float* out3);
@@ -80,9 +81,11 @@ void gn_matvec(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int d
   };
   if (mode == 0) spectral_regop(ctx, s, vt3, beta, false, false, reg);
   if (mode == 1) side_regop();
-  sl_inc_state(ctx, s, disp3, flags, degree, grads, vt3, nullptr, psi + size_t(s.nt) * N);
+  // the inc-state steps also zero psi's slices 0..nt-1, the transpose
+  // sweeps' accumulation targets
+  sl_inc_state(ctx, s, disp3, flags, degree, grads, vt3, nullptr, psi + size_t(s.nt) * N, psi);
   if (mode == 2) side_regop();
-  sl_transpose_sweeps(ctx, s, disp3, flags, degree, psi);
+  sl_transpose_sweeps(ctx, s, disp3, flags, degree, psi, true);
   if (mode != 0) VB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
   sl_assemble(ctx, s, 1, psi, grads, reg, out3);
 }

@@ -909,7 +909,8 @@ inline const float* gather_source(vreg_ctx ctx, const Slab& s, int degree, const
 template <int MODE>
 void gather_pipe(vreg_ctx ctx, const Slab& s, int degree, bool dist, const float* f,
                  const Ghosts& gh, const int* boxes, const float* disp3, const float* aux,
-                 float* out, float half, int last, float* mt_out, TileZ zm, int nz) {
+                 float* out, float half, int last, float* mt_out, TileZ zm, int nz,
+                 float* zero_out = nullptr) {
   const Geo g = geo_of(s);
   const CUtensorMap tmD = tmap_planes(disp3, s, 3 * s.n1l);
   const CUtensorMap tmA = aux ? tmap_planes(aux, s, s.n1l) : tmD;
@@ -928,7 +929,7 @@ void gather_pipe(vreg_ctx ctx, const Slab& s, int degree, bool dist, const float
               (pipe_kernel(k_gather_pipe<DEG, DIST, MODE>)<<<grid, PIPE_THREADS, PIPE_SMEM,
                                                              ctx->stream>>>(
                   g, src_of<DIST>(f, gh), boxes, tmD, tmA, aux ? 1 : 0, out, half, last, mt_out,
-                  zm, pt, sched)));
+                  zm, pt, sched, zero_out)));
 }
 
 struct CharsInfo {
@@ -992,7 +993,7 @@ void interp_sweep(vreg_ctx ctx, const Slab& s, const float* f, const float* disp
 // receives max|out| bits for a following sweep.
 void scatter_sweep(vreg_ctx ctx, const Slab& s, const float* z, const float* disp3,
                    const CharsInfo& ci, int degree, float* out, unsigned* zmax = nullptr,
-                   unsigned* next_max = nullptr) {
+                   unsigned* next_max = nullptr, bool prezeroed = false) {
   const size_t N = s.local();
   if (ci.identity) {
     if (out != z)
@@ -1012,7 +1013,7 @@ void scatter_sweep(vreg_ctx ctx, const Slab& s, const float* z, const float* dis
   Timed t(ctx, T_SL, "sl_scatter_sweep");
   const Geo g = geo_of(s);
   if (!ctx->deterministic) {
-    VB_CUDA(cudaMemsetAsync(out, 0, N * sizeof(float), ctx->stream));
+    if (!prezeroed) VB_CUDA(cudaMemsetAsync(out, 0, N * sizeof(float), ctx->stream));
     const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
     scatter_tiles(ctx, s, acc, out, dist, [&](TileZ zm, int nz) {
       SL_DISPATCH(degree, dist,
@@ -1074,7 +1075,8 @@ void sl_scatter(vreg_ctx ctx, const Slab& s, const float* z, const float* disp3,
 }
 
 void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, int degree,
-                  const float* grads, const float* vt3, float* mt_all, float* psi_out) {
+                  const float* grads, const float* vt3, float* mt_all, float* psi_out,
+                  float* zero_slices) {
   check_degree(degree);
   const CharsInfo ci = chars_info(ctx, s, disp3, flags, degree);
   const size_t N = s.local();
@@ -1101,6 +1103,13 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
     check_launch();
   }
   if (mt_all) VB_CUDA(cudaMemsetAsync(mt_all, 0, N * sizeof(float), ctx->stream));
+  // zero_slices (the transpose sweeps' outputs, nt slices): the pipeline
+  // steps store the zeros next to their outputs (an HBM write in LSU-bound
+  // sweeps instead of a memset per transpose sweep); other paths memset here
+  if (zero_slices && !(fused_u && use_pipe(s, {w, w + N, disp3, u, psi_out, mt_all}))) {
+    VB_CUDA(cudaMemsetAsync(zero_slices, 0, size_t(nt) * N * sizeof(float), ctx->stream));
+    zero_slices = nullptr;
+  }
   const bool dist = ctx->nranks > 1 && !ci.identity;
   const Geo g = geo_of(s);
   const dim3 grid = sl_grid(s), block(BX, BY);
@@ -1122,10 +1131,12 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
       const TileLaunch tl = tile_table(ctx, s, disp3, degree, false);
       const float* ut = u + size_t(t) * N;
       const bool pipe = use_pipe(s, {src, disp3, ut, wn, mo});
+      float* zo = zero_slices ? zero_slices + size_t(t) * N : nullptr;
+      if (zo && !pipe) VB_CUDA(cudaMemsetAsync(zo, 0, N * sizeof(float), ctx->stream));
       gather_tiles(ctx, s, src, ci.G, dist, gh, [&](TileZ zm, int nz) {
         if (pipe) {
           gather_pipe<2>(ctx, s, degree, dist, src, gh, tl.boxes, disp3, ut, wn, half,
-                         last ? 1 : 0, mo, zm, nz);
+                         last ? 1 : 0, mo, zm, nz, zo);
           return;
         }
         SL_DISPATCH(degree, dist,
@@ -1149,7 +1160,7 @@ void sl_inc_state(vreg_ctx ctx, const Slab& s, const float* disp3, int flags, in
 
 // psi[t-1] = I^T psi[t] for t = nt..1; psi holds nt+1 slices, psi[nt] set.
 void sl_transpose_sweeps(vreg_ctx ctx, const Slab& s, const float* disp3, int flags,
-                         int degree, float* psi) {
+                         int degree, float* psi, bool prezeroed) {
   check_degree(degree);
   const CharsInfo ci = chars_info(ctx, s, disp3, flags, degree);
   const size_t N = s.local();
@@ -1167,7 +1178,7 @@ void sl_transpose_sweeps(vreg_ctx ctx, const Slab& s, const float* disp3, int fl
   }
   for (int t = s.nt; t > 0; --t)
     scatter_sweep(ctx, s, psi + size_t(t) * N, disp3, ci, degree, psi + size_t(t - 1) * N,
-                  mx ? mx + t : nullptr, mx && t > 1 ? mx + t - 1 : nullptr);
+                  mx ? mx + t : nullptr, mx && t > 1 ? mx + t - 1 : nullptr, prezeroed);
 }
 
 // psi buffer ((nt+1) slices) of a GN matvec
@@ -1328,7 +1339,7 @@ int vreg_inc_state(vreg_ctx ctx, const vreg_grid* g, const float* disp3, int ide
     Slab s = slab_of(ctx, g);
     const size_t N = s.local();
     float* psi = static_cast<float*>(workspace(ctx, "inc_psi", N * sizeof(float)));
-    sl_inc_state(ctx, s, disp3, identity, degree, grads, vt3, mt_all, psi);
+    sl_inc_state(ctx, s, disp3, identity, degree, grads, vt3, mt_all, psi, nullptr);
     if (mt_final) {  // psi_nt = -m~_nt
       VB_CUDA(cudaMemcpyAsync(mt_final, psi, N * sizeof(float), cudaMemcpyDeviceToDevice,
                               ctx->stream));
@@ -1347,7 +1358,7 @@ int vreg_transpose_assemble(vreg_ctx ctx, const vreg_grid* g, const float* disp3
         workspace(ctx, "mv_psi", size_t(s.nt + 1) * N * sizeof(float)));
     VB_CUDA(cudaMemcpyAsync(psi + size_t(s.nt) * N, fin, N * sizeof(float),
                             cudaMemcpyDeviceToDevice, ctx->stream));
-    sl_transpose_sweeps(ctx, s, disp3, identity, degree, psi);
+    sl_transpose_sweeps(ctx, s, disp3, identity, degree, psi, false);
     sl_assemble(ctx, s, 1, psi, grads, nullptr, out3);
   });
 }

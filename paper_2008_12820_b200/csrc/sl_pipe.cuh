@@ -256,7 +256,8 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1)
     k_gather_pipe(Geo g, SrcField<DIST> src, const int* __restrict__ boxes,
                   const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmA,
                   int has_aux, float* __restrict__ out, float half, int last,
-                  float* __restrict__ mt_out, TileZ zm, PipeTiles pt, int* __restrict__ sched) {
+                  float* __restrict__ mt_out, TileZ zm, PipeTiles pt, int* __restrict__ sched,
+                  float* __restrict__ zero_out) {
   extern __shared__ __align__(128) float pipe_raw[];
   __shared__ int next_tile;
   __shared__ __align__(8) uint64_t full[PIPE_STAGES], empty[PIPE_STAGES];
@@ -346,6 +347,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1)
         const float m = G - half * u;
         if (mt_out) mt_out[p] = m;
         out[p] = last ? -m : m - half * u;
+        if (zero_out) zero_out[p] = 0.0f;  // a transpose sweep's output, pre-zeroed here
       }
     }
     __syncwarp();
